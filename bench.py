@@ -1,0 +1,492 @@
+#!/usr/bin/env python3
+"""Benchmark harness: GDOF/s and % of the empirical HBM roofline for the
+BP1.0 / BP3.5 / BP3.0 FP64 element matvecs at N=7 (BASELINE.json metric).
+
+One *step* = one apply of the operator over the whole synthetic element
+batch resident in HBM.  Headline workload (N=1): BASELINE configs[1], BP3.5
+N=7 E=32768 -- 1.21 GB of algorithmic traffic per apply, so the inputs are
+larger than L2 between timed iterations.  BP1.0 (config 1, E=4096, 57 MB)
+and BP3.0 (config 3, E=32768) are reported under ``per_bp``; the L2-resident
+BP1.0 config is timed with an L2 flush before every apply.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Under torchrun each rank owns its own E-element shard (weak scaling, no
+data-path collective); the reported time is the max over ranks.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "GDOF/s and % empirical HBM roofline, BP1.0/3.5/3.0 FP64 N=7, 1/2/4/8 B200"
+DEGREE = 7
+LAM = 1.0
+HEADLINE = ("BP3.5", 32)          # configs[1]: side 32 -> E = 32768
+EXTRA = (("BP1.0", 16), ("BP3.0", 32), ("BP1.0", 32))
+SAMPLE_EL = 2048                  # CPU-baseline sample (elements)
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# clocks
+# ---------------------------------------------------------------------------
+
+REASONS = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        q = "clocks.sm,clocks.max.sm," + ",".join(f"clocks_event_reasons.{r}" for r in REASONS)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 2 + len(REASONS):
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for r, v in zip(REASONS, parts[2:]):
+                if v.lower() == "active":
+                    reasons.add(r)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+
+def dist_setup(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(value, world):
+    if world == 1:
+        return value
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(value, world):
+    if world == 1:
+        return value
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def build_operator(bp, side, rank):
+    import paper_1711_00903_b200 as hx
+
+    mesh = hx.perturb_mesh(hx.build_cube_mesh(side, 2.0), amplitude=0.15, seed=7 + rank)
+    op = hx.make_operator(bp, DEGREE, mesh, lam=LAM)
+    return mesh, op
+
+
+def copy_bandwidth(nbytes, trials=10):
+    """Paper's empirical roofline: D2D copy of copy_equivalent_bytes, one
+    warm-up, mean of `trials`; read+write bytes counted."""
+    import torch
+
+    n = max(1, nbytes // 8)
+    a = torch.randn(n, dtype=torch.float64, device="cuda")
+    b = torch.empty_like(a)
+    b.copy_(a)
+    rates = []
+    for _ in range(trials):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        b.copy_(a)
+        e.record()
+        e.synchronize()
+        rates.append(2 * n * 8 / (s.elapsed_time(e) * 1e-3))
+    del a, b
+    return float(np.mean(rates)), float(np.max(rates))
+
+
+def time_applies(op, q, out, steps, warmup, flush=None):
+    """Per-launch CUDA-event times (ms) on the launching stream."""
+    import torch
+    import paper_1711_00903_b200 as hx
+
+    stream = torch.cuda.current_stream()
+    for _ in range(warmup):
+        hx.apply_device(op, q, out)
+    torch.cuda.synchronize()
+    times = []
+    for _ in range(steps):
+        if flush is not None:
+            flush.add_(1.0)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        hx.apply_device(op, q, out)
+        e.record(stream)
+        times.append((s, e))
+    torch.cuda.synchronize()
+    return [s.elapsed_time(e) for s, e in times]
+
+
+def bp_report(bp, side, rank, steps, warmup, hbm_peak):
+    import torch
+    import paper_1711_00903_b200 as hx
+
+    mesh, op = build_operator(bp, side, rank)
+    q = hx.FieldVector.random(mesh.n_el, op.n_p, seed=0).to_device().data
+    out = torch.empty_like(q)
+    t = hx.traffic(bp, DEGREE, mesh.n_el)
+    bytes_per_apply = t.bytes_per_element * mesh.n_el
+    flops = hx.flop_model(bp, "fused", DEGREE) * mesh.n_el
+    l2_resident = bytes_per_apply < 256e6
+    flush = torch.zeros(64 << 20, dtype=torch.float64, device="cuda") if l2_resident else None
+    ms = time_applies(op, q, out, steps, warmup, flush)
+    med = statistics.median(ms)
+    mean = statistics.mean(ms)
+    b_copy_mean, b_copy_best = copy_bandwidth(t.copy_equivalent_bytes)
+    rep = {
+        "bp": bp, "degree": DEGREE, "n_el": mesh.n_el, "lam": LAM,
+        "kernel_ms_median": med, "kernel_ms_mean": mean,
+        "gdof_per_s": mesh.n_el * op.n_p / (med * 1e-3) / 1e9,
+        "gflop_per_s": flops / (med * 1e-3) / 1e9,
+        "achieved_gb_per_s": bytes_per_apply / (med * 1e-3) / 1e9,
+        "bytes_per_apply": bytes_per_apply,
+        "frac_of_measured_peak": bytes_per_apply / (med * 1e-3) / 1e9 / hbm_peak,
+        "b_copy_same_size_gb_per_s": b_copy_mean / 1e9,
+        "b_copy_same_size_best_gb_per_s": b_copy_best / 1e9,
+        "frac_of_copy_same_size": bytes_per_apply / (med * 1e-3) / b_copy_mean,
+        "l2": "flushed before every apply" if l2_resident else "inputs larger than L2",
+        "threads": op.plan.threads, "elements_per_tile": op.plan.elements_per_tile,
+        "smem_bytes": op.plan.smem_bytes,
+    }
+    if l2_resident:
+        hot = time_applies(op, q, out, steps, warmup, None)
+        rep["l2_resident_back_to_back_gdof_per_s"] = \
+            mesh.n_el * op.n_p / (statistics.median(hot) * 1e-3) / 1e9
+    del op, q, out, flush
+    torch.cuda.empty_cache()
+    return rep
+
+
+def cpu_baseline(bp=HEADLINE[0]):
+    """Oracle port (numpy restatement of the reference apply) on a bounded
+    sample of the headline workload, BLAS pinned to one thread."""
+    import paper_1711_00903_b200 as hx
+    from oracle import hexbench_oracle as orc
+    try:
+        from threadpoolctl import threadpool_limits
+    except ImportError:  # pragma: no cover
+        threadpool_limits = None
+
+    mesh = hx.perturb_mesh(hx.build_cube_mesh(HEADLINE[1], 2.0), amplitude=0.15, seed=7)
+    sub = hx.HexMesh(SAMPLE_EL, mesh.vertices[:SAMPLE_EL], mesh.extent)
+    op = hx.make_operator(bp, DEGREE, sub, lam=LAM)
+    fac = op.factors.data
+    q = np.random.default_rng(0).standard_normal((SAMPLE_EL, op.n_p))
+    interp = None if op.interp is None else op.interp.entries
+    diff = None if op.diff is None else op.diff.entries
+    ctx = threadpool_limits(1) if threadpool_limits else None
+    if ctx:
+        ctx.__enter__()
+    try:
+        orc.apply_chunked(bp, DEGREE, LAM, interp, diff, fac, q)
+        reps, t0 = 0, time.perf_counter()
+        while True:
+            orc.apply_chunked(bp, DEGREE, LAM, interp, diff, fac, q)
+            reps += 1
+            el = time.perf_counter() - t0
+            if el > 10.0 or reps >= 200:
+                break
+    finally:
+        if ctx:
+            ctx.__exit__(None, None, None)
+    per = el / reps
+    return {"value": SAMPLE_EL * op.n_p / per / 1e9, "unit": "GDOF/s", "cores": 1,
+            "kind": "port",
+            "sample": f"{bp} N={DEGREE} first {SAMPLE_EL} elements of the E=32768 mesh, "
+                      f"{reps} applies in {el:.1f} s (oracle/hexbench_oracle.py, numpy, "
+                      "1 BLAS thread)"}
+
+
+def e2e_report(op, mesh, steps, warmup):
+    """Same metric through the public host-buffer API (hx_apply_host): per step
+    the H2D copy of q from pinned memory, the kernel and the D2H copy of out."""
+    import torch
+    import paper_1711_00903_b200 as hx
+
+    n = mesh.n_el * op.n_p
+    q_pin = torch.empty(n, dtype=torch.float64).pin_memory()
+    q_pin.copy_(torch.from_numpy(np.random.default_rng(0).standard_normal(n)))
+    o_pin = torch.empty(n, dtype=torch.float64).pin_memory()
+    qh, oh = q_pin.numpy(), o_pin.numpy()
+    chunk = hx.operators.host_chunk_elements(op)
+    from paper_1711_00903_b200 import _native
+    nbytes = _native.lib().hx_apply_host_workspace(op.plan.handle, chunk)
+    work = torch.empty(nbytes // 8, dtype=torch.float64, device="cuda")
+    stream = torch.cuda.current_stream()
+    for _ in range(warmup):
+        hx.apply_host(op, qh, oh, chunk_el=chunk, work=work)
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record(stream)
+    for _ in range(steps):
+        hx.apply_host(op, qh, oh, chunk_el=chunk, work=work)
+    e.record(stream)
+    e.synchronize()
+    ms = s.elapsed_time(e) / steps
+    return ms, {"value": None, "unit": "GDOF/s", "h2d_bytes_per_step": n * 8,
+                "d2h_bytes_per_step": n * 8, "ms_per_step": ms,
+                "path": "hx_apply_host (C ABI), pinned host q/out, chunked 3-stream "
+                        f"H2D/kernel/D2H pipeline, chunk {chunk} elements"}
+
+
+def run_ours(args):
+    import torch
+    import paper_1711_00903_b200 as hx
+
+    rank, world, local = dist_setup(args)
+    hbm_peak, peak_kind = load_peaks()
+    bp, side = HEADLINE
+    mesh, op = build_operator(bp, side, rank)
+    q = hx.FieldVector.random(mesh.n_el, op.n_p, seed=0).to_device().data
+    out = torch.empty_like(q)
+    t = hx.traffic(bp, DEGREE, mesh.n_el)
+    bytes_per_apply = t.bytes_per_element * mesh.n_el
+    stream = torch.cuda.current_stream()
+
+    for _ in range(args.warmup):
+        hx.apply_device(op, q, out)
+    torch.cuda.synchronize()
+    barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        start = torch.cuda.Event(enable_timing=True)
+        stop = torch.cuda.Event(enable_timing=True)
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(args.steps)]
+        start.record(stream)
+        for s, e in ev:
+            s.record(stream)
+            hx.apply_device(op, q, out)
+            e.record(stream)
+        stop.record(stream)
+        torch.cuda.synchronize()
+    barrier(world)
+    total_ms = max_over_ranks(start.elapsed_time(stop), world)
+    kernel_ms = statistics.mean(s.elapsed_time(e) for s, e in ev)
+    kernel_ms = max_over_ranks(kernel_ms, world)
+    ms_per_step = total_ms / args.steps
+    dofs_all = sum_over_ranks(mesh.n_el * op.n_p, world)
+    value = dofs_all / (ms_per_step * 1e-3) / 1e9
+    achieved = bytes_per_apply / (kernel_ms * 1e-3) / 1e9
+
+    e2e_ms, e2e = e2e_report(op, mesh, max(3, args.steps // 4), 2)
+    e2e_ms = max_over_ranks(e2e_ms, world)
+    e2e["value"] = dofs_all / (e2e_ms * 1e-3) / 1e9
+    e2e["ms_per_step"] = e2e_ms
+
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as fh:
+            traffic = json.load(fh).get("bp35_kernel<7>")
+
+    per_bp = {}
+    cpu = None
+    del op, q, out
+    torch.cuda.empty_cache()
+    if rank == 0 and world == 1 and not args.quick:
+        per_bp[f"{bp} E={mesh.n_el}"] = bp_report(bp, side, 0, args.steps, args.warmup, hbm_peak)
+        for xbp, xside in EXTRA:
+            r = bp_report(xbp, xside, 0, args.steps, args.warmup, hbm_peak)
+            per_bp[f"{xbp} E={r['n_el']}"] = r
+        cpu = cpu_baseline()
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GDOF/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic: perturb_mesh(build_cube_mesh(32, 2.0), 0.15, seed=7+rank), "
+                    "q = FieldVector.random(seed=0), device-generated geometric factors",
+            "config": {"workload": f"{bp} N={DEGREE} E={mesh.n_el} per GPU (BASELINE configs[1])",
+                       "bp": bp, "degree": DEGREE, "n_el_per_gpu": mesh.n_el, "lam": LAM,
+                       "l2": "inputs larger than L2 (1.21 GB per apply)",
+                       "parallelism": f"element partition x{world}, no data-path collective"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak,
+                         "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": traffic,
+                         "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)"
+                         if peak_kind == "measured" else "fallback 6650 GB/s",
+                         "kernel": f"bp35_kernel<{DEGREE}>",
+                         "algorithmic_bytes_per_element": t.bytes_per_element,
+                         "kernel_ms": kernel_ms},
+            "e2e": e2e,
+            "gpu_launches": args.steps,
+            "clocks": clocks.summary(),
+            "cpu_baseline": cpu,
+            "per_bp": per_bp,
+            "gflop_per_s": hx.flop_model(bp, "fused", DEGREE) * dofs_all / (DEGREE + 1) ** 3
+                           / (ms_per_step * 1e-3) / 1e9,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the oracle port on the host cores
+# ---------------------------------------------------------------------------
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from concurrent.futures import ThreadPoolExecutor
+
+    import paper_1711_00903_b200 as hx
+    from oracle import hexbench_oracle as orc
+
+    bp, side = HEADLINE
+    cores = os.cpu_count() or 1
+    sample = 4096
+    mesh = hx.perturb_mesh(hx.build_cube_mesh(side, 2.0), amplitude=0.15, seed=7)
+    sub = hx.HexMesh(sample, mesh.vertices[:sample], mesh.extent)
+    fac = hx.geometric_factors(sub, hx.gll_rule(DEGREE + 1) if bp == "BP3.5"
+                               else hx.gl_rule(DEGREE + 2)).data
+    diff = hx.diff_matrix_gll(DEGREE).entries
+    q = np.random.default_rng(0).standard_normal((sample, (DEGREE + 1) ** 3))
+    chunks = np.linspace(0, sample, cores + 1).astype(int)
+
+    def work(rng):
+        lo, hi = rng
+        return orc.apply(bp, DEGREE, LAM, None, diff, fac[lo:hi], q[lo:hi])
+
+    pool = ThreadPoolExecutor(max_workers=cores)
+    spans = [(lo, hi) for lo, hi in zip(chunks[:-1], chunks[1:]) if hi > lo]
+
+    def step():
+        list(pool.map(work, spans))
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    el = time.perf_counter() - t0
+    ms = el / args.steps * 1e3
+    value = sample * q.shape[1] / (ms * 1e-3) / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": "GDOF/s", "n_gpus": 0,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "impl": "reference",
+        "data": "synthetic: same mesh / q generator as the GPU arm",
+        "config": {"workload": f"{bp} N={DEGREE} E=32768 (BASELINE configs[1]), "
+                               f"bounded sample of {sample} elements per step",
+                   "bp": bp, "degree": DEGREE, "lam": LAM},
+        "cpu_baseline": {"value": value, "unit": "GDOF/s", "cores": cores, "kind": "port",
+                         "sample": f"first {sample} elements, {cores} threads over element "
+                                   "ranges, oracle/hexbench_oracle.py (numpy)"},
+        "e2e": {"value": value, "unit": "GDOF/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--quick", action="store_true",
+                    help="headline only (skip per-BP reports and the CPU baseline)")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

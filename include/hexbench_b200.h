@@ -1,0 +1,117 @@
+/*
+ * hexbench_b200 -- C ABI of the B200-native BP1.0 / BP3.5 / BP3.0 element matvecs.
+ *
+ * The reference (`hexbench`, /root/reference/pkg) is pure Python and has no
+ * FFI; these entry points are what its operator layer binds to when the
+ * per-element numpy loop is replaced by sm_100a kernels.  Each function cites
+ * the reference interface it stands in for.  Plain pointers and sizes only:
+ * device buffers belong to the caller (PyTorch tensors in the Python layer),
+ * the plan owns only its copy of the 1-D matrices.
+ *
+ * Conventions
+ *   - fields q / out: element-major (n_el, (N+1)^3) float64, point order
+ *     (k, j, i) with i fastest -- identical to FieldVector.data
+ *     (reference operators.py:67-79).
+ *   - factors: packed device layout, per element `n_slots` slots of
+ *     `slot_stride` doubles (see hx_plan_factor_layout).  Slot order is the
+ *     reference's FACTOR_NAMES (mesh.py:12); BP1.0 keeps only GwJ.
+ *   - every call that takes a `stream` is asynchronous on that cudaStream_t
+ *     (NULL = legacy default stream) and never synchronises the device.
+ *   - status: 0 on success, otherwise an HX_E* code; hx_strerror explains it.
+ */
+#ifndef HEXBENCH_B200_H
+#define HEXBENCH_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  HX_OK = 0,
+  HX_EINVAL = 1,       /* bad argument: maps to ValueError */
+  HX_ENONFINITE = 2,   /* q holds inf/nan: ValueError (operators.py:317-318) */
+  HX_EDEGENERATE = 3,  /* non-positive Jacobian: DegenerateGeometryError (mesh.py:128-129) */
+  HX_ECUDA = 4,        /* CUDA runtime failure: RuntimeError */
+  HX_ENOMEM = 5        /* host allocation failed */
+};
+
+/* benchmark ids (reference operators.py:30-33: "BP1.0", "BP3.5", "BP3.0") */
+enum { HX_BP1 = 10, HX_BP35 = 35, HX_BP3 = 30 };
+
+/* flag bits the kernels OR into *status_flag */
+enum { HX_FLAG_NONFINITE = 1, HX_FLAG_DEGENERATE = 2 };
+
+typedef struct hx_plan hx_plan;
+
+/* Replaces the matrix / rule selection of make_operator (operators.py:118-143).
+ *   interp : (N+2) x (N+1) row-major I            (BP1.0, BP3.0; NULL for BP3.5)
+ *   diff   : q x q row-major D (q=N+1) or D~ (q=N+2) (BP3.5, BP3.0; NULL for BP1.0)
+ *   nodes, weights : the q-point rule the factors live on (GL N+2 for BP1.0/3.0,
+ *                    GLL N+1 for BP3.5)
+ * Validation mirrors operators.py:120-129 (unknown bp, lam < 0, degree 1..15).
+ * Touches no device state.                                                  */
+int hx_plan_create(int bp, int degree, double lam, const double* interp, const double* diff,
+                   const double* nodes, const double* weights, hx_plan** out);
+
+/* Releases the plan (and any streams/events hx_apply_host created). */
+void hx_plan_destroy(hx_plan* plan);
+
+/* Packed factor layout of the plan: slots per element, doubles per slot and
+ * doubles per element (= n_slots * slot_stride).                            */
+int hx_plan_factor_layout(const hx_plan* plan, int* n_slots, int64_t* slot_stride,
+                          int64_t* element_stride);
+
+/* Replaces geometric_factors (mesh.py:101-139) for the plan's rule, on device.
+ *   vertices : device (n_el, 8, 3) float64 corner coordinates (HexMesh.vertices)
+ *   all_slots: 0 -> the plan's packed layout; 1 -> all 7 slots with the same
+ *              slot_stride (used to materialise the reference array)
+ *   status_flag: device int; HX_FLAG_DEGENERATE is OR-ed in if det <= 1e-14  */
+int hx_geometric_factors(const hx_plan* plan, const double* vertices, int64_t n_el,
+                         int all_slots, double* factors, int* status_flag, void* stream);
+
+/* Converts between the reference factor layout (n_el, 7, q^3) and the packed
+ * layout, device to device.  to_packed = 1: ref -> packed, 0: packed(7 slots)
+ * -> ref.                                                                    */
+int hx_repack_factors(const hx_plan* plan, const double* src, int64_t n_el, double* dst,
+                      int to_packed, void* stream);
+
+/* Replaces apply_operator / apply_bp1 / apply_bp35 / apply_bp3
+ * (operators.py:306-349) on device-resident data: out = A q for elements
+ * [0, n_el).  One fused kernel launch; no allocation, no synchronisation.
+ * status_flag (device int, may be NULL) receives HX_FLAG_NONFINITE if any q
+ * entry is inf/nan (the reference's np.isfinite scan, fused into the load). */
+int hx_apply(const hx_plan* plan, const double* q, const double* factors, double* out,
+             int64_t n_el, int* status_flag, void* stream);
+
+/* End-to-end variant on HOST q / out (page-locked for full overlap): chunks of
+ * `chunk_el` elements are copied in, applied and copied back on a three-stream
+ * pipeline so PCIe transfers overlap the kernel.  `work` is a device buffer of
+ * at least hx_apply_host_workspace(plan, chunk_el) bytes; `stream` is made to
+ * wait for the whole pipeline.                                              */
+int64_t hx_apply_host_workspace(const hx_plan* plan, int64_t chunk_el);
+int hx_apply_host(const hx_plan* plan, const double* q_host, const double* factors,
+                  double* out_host, int64_t n_el, int64_t chunk_el, void* work,
+                  int* status_flag, void* stream);
+
+/* Elements each CTA processes per tile, threads per CTA and dynamic shared
+ * memory bytes of the plan's kernel (for reports and tests).                */
+int hx_plan_kernel_shape(const hx_plan* plan, int* elements_per_tile, int* threads,
+                         int* smem_bytes);
+
+/* Shared-memory bandwidth probe (harness calibration replacing the B_sh
+ * ansatz, perf.py:155-160): fills *bytes_per_s with the measured aggregate
+ * LDS bandwidth of the current device.  Synchronises `stream`.              */
+int hx_measure_smem_bandwidth(double* bytes_per_s, void* stream);
+
+const char* hx_strerror(int status);
+
+/* 1 if the library was built for (and the current device is) sm_100. */
+int hx_device_ok(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HEXBENCH_B200_H */

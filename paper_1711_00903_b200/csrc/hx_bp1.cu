@@ -1,0 +1,204 @@
+// BP1.0 -- mass matvec with de-aliased Gauss quadrature (reference
+// operators.py:274-281):  out = I^T ( GwJ * I q ),  I: GLL(n) -> GL(m).
+//
+// Persistent CTAs over tiles of EPB elements, one 1-D line per thread,
+// per-element tensors in padded shared memory (hx_layouts.h phases X, Y):
+//
+//   S1 j-lines (k,i)  n^2 : q (HBM, 8n-byte runs) -> I_s -> X[k][a][i]
+//   S2 i-lines (k,a)  n*m : X -> I_r -> Y[k][a][c]
+//   S3 k-lines (a,c)  m^2 : Y -> I_t -> * GwJ (HBM, coalesced) -> I_t^T -> Y (in place)
+//   S4 i-lines (k,a)  n*m : Y -> I_r^T -> X[k][a][i]
+//   S5 j-lines (k,i)  n^2 : X -> I_s^T -> out (HBM)
+//
+// The k-direction interpolation, the GwJ scaling and the k-direction
+// projection are fused in registers in S3, so the GL-point tensor never
+// leaves the thread that owns its k-line.  The contraction order differs from
+// the reference's (j, i, k) only by floating-point reassociation.
+#include "hx_common.cuh"
+#include "hx_plan.h"
+
+namespace hx {
+
+template <int N>
+struct BP1Params {
+  Fold<N + 2, N + 1> I;   // GLL -> GL interpolation (centro-symmetric)
+  Fold<N + 1, N + 2> It;  // its transpose (projection)
+  const double* q;
+  const double* gwj;
+  double* out;
+  int64_t n_el;
+  int64_t fac_estride;
+  int* flag;
+};
+
+template <int N>
+__global__ void __launch_bounds__(Cfg<kBP1, N>::NT)
+    bp1_kernel(const __grid_constant__ BP1Params<N> p) {
+  using C = Cfg<kBP1, N>;
+  constexpr int n = N + 1, m = N + 2, n2 = n * n, n3 = n2 * n, m2 = m * m;
+  constexpr int EPB = C::EPB;
+  constexpr Lay LX = C::L[0], LY = C::L[1];
+  constexpr int EX = C::EBUF[0], EY = C::EBUF[1];
+  extern __shared__ double smem[];
+  double* const X = smem;
+  double* const Y = X + EPB * EX;
+
+  const int tid = threadIdx.x;
+  const int64_t ntiles = (p.n_el + EPB - 1) / EPB;
+  const int64_t fs = p.fac_estride;
+
+  if (tid == 0 && blockIdx.x < ntiles) {
+    const int64_t e0 = int64_t(blockIdx.x) * EPB;
+    const int64_t ne = min64(EPB, p.n_el - e0);
+    prefetch_l2(p.q + e0 * n3, ne * n3 * sizeof(double));
+    prefetch_l2(p.gwj + e0 * fs, ne * fs * sizeof(double));
+  }
+
+  // line ownership per stage shape
+  const int el_a = tid / n2, ln_a = tid % n2;  // n^2 lines (S1, S5)
+  const int el_b = tid / (n * m), ln_b = tid % (n * m);  // n*m lines (S2, S4)
+  const int el_c = tid / m2, ln_c = tid % m2;  // m^2 lines (S3)
+
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t e0 = tile * EPB;
+    const int ne = int(min64(EPB, p.n_el - e0));
+    if (tid == 0) {
+      const int64_t nt = tile + gridDim.x;
+      if (nt < ntiles) {
+        const int64_t f0 = nt * EPB;
+        const int64_t nn = min64(EPB, p.n_el - f0);
+        prefetch_l2(p.q + f0 * n3, nn * n3 * sizeof(double));
+        prefetch_l2(p.gwj + f0 * fs, nn * fs * sizeof(double));
+      }
+    }
+    // GwJ of this thread's S3 k-line, issued early so its latency hides
+    // behind S1 and S2.
+    double w[m];
+    if (el_c < ne) {
+      const double* g = p.gwj + (e0 + el_c) * fs + ln_c;
+#pragma unroll
+      for (int c = 0; c < m; ++c) w[c] = g[c * m2];
+    }
+    // ---- S1: j-lines (k, i): interpolate along s
+    if (el_a < ne) {
+      const int k = ln_a / n, i = ln_a % n;
+      const double* src = p.q + (e0 + el_a) * n3 + k * n2 + i;
+      double x[n], y[m];
+      bool bad = false;
+#pragma unroll
+      for (int t = 0; t < n; ++t) {
+        x[t] = src[t * n];
+        bad |= nonfinite(x[t]);
+      }
+      if (bad && p.flag) atomicOr(p.flag, 1);
+      fold_apply<m, n, 1>(p.I, x, y);
+      double* dst = X + el_a * EX + k * LX.s0 + i;
+#pragma unroll
+      for (int t = 0; t < m; ++t) dst[t * LX.s1] = y[t];
+    }
+    __syncthreads();
+    // ---- S2: i-lines (k, a): interpolate along r
+    if (el_b < ne) {
+      const int k = ln_b / m, a = ln_b % m;
+      const double* src = X + el_b * EX + k * LX.s0 + a * LX.s1;
+      double x[n], y[m];
+#pragma unroll
+      for (int t = 0; t < n; ++t) x[t] = src[t];
+      fold_apply<m, n, 1>(p.I, x, y);
+      double* dst = Y + el_b * EY + k * LY.s0 + a * LY.s1;
+#pragma unroll
+      for (int t = 0; t < m; ++t) dst[t] = y[t];
+    }
+    __syncthreads();
+    // ---- S3: k-lines (a, c): interpolate along t, scale, project along t
+    if (el_c < ne) {
+      const int a = ln_c / m, c = ln_c % m;
+      double* line = Y + el_c * EY + a * LY.s1 + c;
+      double x[n], y[m];
+#pragma unroll
+      for (int t = 0; t < n; ++t) x[t] = line[t * LY.s0];
+      fold_apply<m, n, 1>(p.I, x, y);
+#pragma unroll
+      for (int t = 0; t < m; ++t) y[t] *= w[t];
+      fold_apply<n, m, 1>(p.It, y, x);
+#pragma unroll
+      for (int t = 0; t < n; ++t) line[t * LY.s0] = x[t];
+    }
+    __syncthreads();
+    // ---- S4: i-lines (k, a): project along r
+    if (el_b < ne) {
+      const int k = ln_b / m, a = ln_b % m;
+      const double* src = Y + el_b * EY + k * LY.s0 + a * LY.s1;
+      double x[m], y[n];
+#pragma unroll
+      for (int t = 0; t < m; ++t) x[t] = src[t];
+      fold_apply<n, m, 1>(p.It, x, y);
+      double* dst = X + el_b * EX + k * LX.s0 + a * LX.s1;
+#pragma unroll
+      for (int t = 0; t < n; ++t) dst[t] = y[t];
+    }
+    __syncthreads();
+    // ---- S5: j-lines (k, i): project along s and store
+    if (el_a < ne) {
+      const int k = ln_a / n, i = ln_a % n;
+      const double* src = X + el_a * EX + k * LX.s0 + i;
+      double x[m], y[n];
+#pragma unroll
+      for (int t = 0; t < m; ++t) x[t] = src[t * LX.s1];
+      fold_apply<n, m, 1>(p.It, x, y);
+      double* dst = p.out + (e0 + el_a) * n3 + k * n2 + i;
+#pragma unroll
+      for (int t = 0; t < n; ++t) st_stream(dst + t * n, y[t]);
+    }
+    __syncthreads();  // X is rewritten by the next tile's S1
+  }
+}
+
+template <int N>
+static cudaError_t launch_n(const hx_plan& P, const double* q, const double* fac, double* out,
+                            int64_t n_el, int* flag, cudaStream_t s) {
+  using C = Cfg<kBP1, N>;
+  constexpr int n = N + 1, m = N + 2;
+  constexpr int smem = smem_doubles<kBP1, N>() * int(sizeof(double));
+  static int blocks_per_sm = -1;
+  if (blocks_per_sm < 0) {
+    cudaError_t err = cudaFuncSetAttribute(bp1_kernel<N>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (err != cudaSuccess) return err;
+    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, bp1_kernel<N>, C::NT,
+                                                        smem);
+    if (err != cudaSuccess) return err;
+    if (blocks_per_sm < 1) blocks_per_sm = 1;
+  }
+  BP1Params<N> prm;
+  double it[n * m];
+  fill_fold(prm.I, P.interp);
+  transpose(P.interp, m, n, it);
+  fill_fold(prm.It, it);
+  prm.q = q;
+  prm.gwj = fac;
+  prm.out = out;
+  prm.n_el = n_el;
+  prm.fac_estride = P.elem_stride;
+  prm.flag = flag;
+  const int64_t ntiles = (n_el + C::EPB - 1) / C::EPB;
+  const int64_t grid = min64(ntiles, int64_t(blocks_per_sm) * sm_count());
+  bp1_kernel<N><<<unsigned(grid), C::NT, smem, s>>>(prm);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bp1(const hx_plan& P, const double* q, const double* fac, double* out,
+                       int64_t n_el, int* flag, cudaStream_t s) {
+  switch (P.degree) {
+#define HX_CASE(N) \
+  case N:          \
+    return launch_n<N>(P, q, fac, out, n_el, flag, s);
+    HX_CASE(1) HX_CASE(2) HX_CASE(3) HX_CASE(4) HX_CASE(5) HX_CASE(6) HX_CASE(7) HX_CASE(8)
+    HX_CASE(9) HX_CASE(10) HX_CASE(11) HX_CASE(12) HX_CASE(13) HX_CASE(14) HX_CASE(15)
+#undef HX_CASE
+    default:
+      return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace hx

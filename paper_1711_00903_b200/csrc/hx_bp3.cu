@@ -1,0 +1,296 @@
+// BP3.0 -- stiffness matvec with full Gauss quadrature (reference
+// operators.py:287-292):
+//
+//   t   = I q                                   (GLL n^3 -> GL m^3)
+//   a   = lam GwJ t + sum_d D~_d^T ( sum_d' G_dd' D~_d' t )
+//   out = I^T a
+//
+// Persistent CTAs over tiles of EPB elements; one 1-D line per thread; three
+// padded shared-memory buffers A, B, C per element reused across phases
+// (strides: hx_layouts.h, phase order L[0..5] below).
+//
+//   S1 j-lines (k,i)  n^2 : q (HBM)  -> I_s -> A as X[k][a][i]        L[0]
+//   S2 i-lines (k,a)  n*m : X -> I_r -> B as Y[k][a][c]                L[2]
+//   S3 k-lines (a,c)  m^2 : Y -> I_t -> t (regs), tt = D~_t t (regs),
+//                           t -> C as T[kk][a][c]                      L[4]
+//   S4 i-lines (kk,a) m^2 : T -> D~_r -> A as QR                       L[1]
+//      j-lines (kk,c) m^2 : T -> D~_s -> B as QS                       L[3]
+//   S5 k-lines (a,c)  m^2 : G (HBM) chain rule: rqr -> A, rqs -> B,
+//                           acc = lam GwJ t + D~_t^T rqt (regs)
+//   S6 i-lines: A <- D~_r^T A        j-lines: B <- D~_s^T B
+//   S7 k-lines (a,c)  m^2 : acc += A + B;  I_t^T acc -> C as Z[k][a][c] L[5]
+//   S8 i-lines (k,a)  n*m : Z -> I_r^T -> A as W[k][a][i]              L[0]
+//   S9 j-lines (k,i)  n^2 : W -> I_s^T -> out (HBM)
+#include "hx_common.cuh"
+#include "hx_plan.h"
+
+namespace hx {
+
+template <int N>
+struct BP3Params {
+  Fold<N + 2, N + 1> I;
+  Fold<N + 1, N + 2> It;
+  Fold<N + 2, N + 2> D;
+  Fold<N + 2, N + 2> Dt;
+  const double* q;
+  const double* fac;
+  double* out;
+  int64_t n_el;
+  int64_t fac_estride;
+  int64_t fac_sstride;
+  double lam;
+  int* flag;
+};
+
+template <int N>
+__global__ void __launch_bounds__(Cfg<kBP3, N>::NT)
+    bp3_kernel(const __grid_constant__ BP3Params<N> p) {
+  using C = Cfg<kBP3, N>;
+  constexpr int n = N + 1, m = N + 2, n2 = n * n, n3 = n2 * n, m2 = m * m;
+  constexpr int EPB = C::EPB;
+  constexpr Lay LX = C::L[0], LQR = C::L[1], LY = C::L[2], LQS = C::L[3], LT = C::L[4],
+                LZ = C::L[5];
+  constexpr int EA = C::EBUF[0], EB = C::EBUF[1], EC = C::EBUF[2];
+  extern __shared__ double smem[];
+  double* const A = smem;
+  double* const B = A + EPB * EA;
+  double* const Cs = B + EPB * EB;
+
+  const int tid = threadIdx.x;
+  const int64_t ntiles = (p.n_el + EPB - 1) / EPB;
+  const int64_t fs = p.fac_estride, ss = p.fac_sstride;
+
+  if (tid == 0 && blockIdx.x < ntiles) {
+    const int64_t e0 = int64_t(blockIdx.x) * EPB;
+    const int64_t ne = min64(EPB, p.n_el - e0);
+    prefetch_l2(p.q + e0 * n3, ne * n3 * sizeof(double));
+    prefetch_l2(p.fac + e0 * fs, ne * fs * sizeof(double));
+  }
+
+  const int el_a = tid / n2, ln_a = tid % n2;
+  const int el_b = tid / (n * m), ln_b = tid % (n * m);
+  const int el_c = tid / m2, ln_c = tid % m2;
+
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t e0 = tile * EPB;
+    const int ne = int(min64(EPB, p.n_el - e0));
+    if (tid == 0) {
+      const int64_t nt = tile + gridDim.x;
+      if (nt < ntiles) {
+        const int64_t f0 = nt * EPB;
+        const int64_t nn = min64(EPB, p.n_el - f0);
+        prefetch_l2(p.q + f0 * n3, nn * n3 * sizeof(double));
+        prefetch_l2(p.fac + f0 * fs, nn * fs * sizeof(double));
+      }
+    }
+    double* const Aa = A + el_a * EA;
+    double* const Ab = A + el_b * EA;
+    double* const Ac = A + el_c * EA;
+    double* const Bb = B + el_b * EB;
+    double* const Bc = B + el_c * EB;
+    double* const Cb = Cs + el_b * EC;
+    double* const Cc = Cs + el_c * EC;
+
+    // ---- S1: j-lines (k, i): interpolate along s
+    if (el_a < ne) {
+      const int k = ln_a / n, i = ln_a % n;
+      const double* src = p.q + (e0 + el_a) * n3 + k * n2 + i;
+      double x[n], y[m];
+      bool bad = false;
+#pragma unroll
+      for (int t = 0; t < n; ++t) {
+        x[t] = src[t * n];
+        bad |= nonfinite(x[t]);
+      }
+      if (bad && p.flag) atomicOr(p.flag, 1);
+      fold_apply<m, n, 1>(p.I, x, y);
+      double* dst = Aa + k * LX.s0 + i;
+#pragma unroll
+      for (int t = 0; t < m; ++t) dst[t * LX.s1] = y[t];
+    }
+    __syncthreads();
+    // ---- S2: i-lines (k, a): interpolate along r
+    if (el_b < ne) {
+      const int k = ln_b / m, a = ln_b % m;
+      const double* src = Ab + k * LX.s0 + a * LX.s1;
+      double x[n], y[m];
+#pragma unroll
+      for (int t = 0; t < n; ++t) x[t] = src[t];
+      fold_apply<m, n, 1>(p.I, x, y);
+      double* dst = Bb + k * LY.s0 + a * LY.s1;
+#pragma unroll
+      for (int t = 0; t < m; ++t) dst[t] = y[t];
+    }
+    __syncthreads();
+    // ---- S3: k-lines (a, c): interpolate along t, differentiate along t
+    double tv[m], tt[m], acc[m];
+    const bool act_c = el_c < ne;
+    const int ca = ln_c / m, cc = ln_c % m;
+    if (act_c) {
+      const double* src = Bc + ca * LY.s1 + cc;
+      double x[n];
+#pragma unroll
+      for (int t = 0; t < n; ++t) x[t] = src[t * LY.s0];
+      fold_apply<m, n, 1>(p.I, x, tv);
+      fold_apply<m, m, -1>(p.D, tv, tt);
+      double* dst = Cc + ca * LT.s1 + cc;
+#pragma unroll
+      for (int t = 0; t < m; ++t) dst[t * LT.s0] = tv[t];
+    }
+    __syncthreads();
+    // ---- S4: r- and s-derivatives of T
+    if (act_c) {
+      const int kk = ln_c / m, r = ln_c % m;
+      double x[m], y[m];
+      const double* src = Cc + kk * LT.s0 + r * LT.s1;  // i-line (kk, a=r)
+#pragma unroll
+      for (int t = 0; t < m; ++t) x[t] = src[t];
+      fold_apply<m, m, -1>(p.D, x, y);
+      double* dst = Ac + kk * LQR.s0 + r * LQR.s1;
+#pragma unroll
+      for (int t = 0; t < m; ++t) dst[t] = y[t];
+      src = Cc + kk * LT.s0 + r;  // j-line (kk, c=r)
+#pragma unroll
+      for (int t = 0; t < m; ++t) x[t] = src[t * LT.s1];
+      fold_apply<m, m, -1>(p.D, x, y);
+      dst = Bc + kk * LQS.s0 + r;
+#pragma unroll
+      for (int t = 0; t < m; ++t) dst[t * LQS.s1] = y[t];
+    }
+    __syncthreads();
+    // ---- S5: chain rule on k-lines (a, c)
+    if (act_c) {
+      double* qrl = Ac + ca * LQR.s1 + cc;
+      double* qsl = Bc + ca * LQS.s1 + cc;
+      const double* g = p.fac + (e0 + el_c) * fs + ln_c;
+      double rqt[m];
+#pragma unroll
+      for (int t = 0; t < m; ++t) {
+        const double* gk = g + t * m2;
+        const double grr = gk[0], grs = gk[ss], grt = gk[2 * ss];
+        const double gss = gk[3 * ss], gst = gk[4 * ss], gtt = gk[5 * ss];
+        const double gwj = gk[6 * ss];
+        const double qr = qrl[t * LQR.s0], qs = qsl[t * LQS.s0], qt = tt[t];
+        qrl[t * LQR.s0] = grr * qr + grs * qs + grt * qt;
+        qsl[t * LQS.s0] = grs * qr + gss * qs + gst * qt;
+        rqt[t] = grt * qr + gst * qs + gtt * qt;
+        tv[t] = p.lam * gwj * tv[t];
+      }
+      fold_apply<m, m, -1>(p.Dt, rqt, acc);
+#pragma unroll
+      for (int t = 0; t < m; ++t) acc[t] += tv[t];
+    }
+    __syncthreads();
+    // ---- S6: transposed r- and s-derivatives in place
+    if (act_c) {
+      const int kk = ln_c / m, r = ln_c % m;
+      double x[m], y[m];
+      double* l = Ac + kk * LQR.s0 + r * LQR.s1;
+#pragma unroll
+      for (int t = 0; t < m; ++t) x[t] = l[t];
+      fold_apply<m, m, -1>(p.Dt, x, y);
+#pragma unroll
+      for (int t = 0; t < m; ++t) l[t] = y[t];
+      l = Bc + kk * LQS.s0 + r;
+#pragma unroll
+      for (int t = 0; t < m; ++t) x[t] = l[t * LQS.s1];
+      fold_apply<m, m, -1>(p.Dt, x, y);
+#pragma unroll
+      for (int t = 0; t < m; ++t) l[t * LQS.s1] = y[t];
+    }
+    __syncthreads();
+    // ---- S7: combine, project along t
+    if (act_c) {
+      const double* qrl = Ac + ca * LQR.s1 + cc;
+      const double* qsl = Bc + ca * LQS.s1 + cc;
+#pragma unroll
+      for (int t = 0; t < m; ++t) acc[t] += qrl[t * LQR.s0] + qsl[t * LQS.s0];
+      double y[n];
+      fold_apply<n, m, 1>(p.It, acc, y);
+      double* dst = Cc + ca * LZ.s1 + cc;
+#pragma unroll
+      for (int t = 0; t < n; ++t) dst[t * LZ.s0] = y[t];
+    }
+    __syncthreads();
+    // ---- S8: i-lines (k, a): project along r
+    if (el_b < ne) {
+      const int k = ln_b / m, a = ln_b % m;
+      const double* src = Cb + k * LZ.s0 + a * LZ.s1;
+      double x[m], y[n];
+#pragma unroll
+      for (int t = 0; t < m; ++t) x[t] = src[t];
+      fold_apply<n, m, 1>(p.It, x, y);
+      double* dst = Ab + k * LX.s0 + a * LX.s1;
+#pragma unroll
+      for (int t = 0; t < n; ++t) dst[t] = y[t];
+    }
+    __syncthreads();
+    // ---- S9: j-lines (k, i): project along s and store
+    if (el_a < ne) {
+      const int k = ln_a / n, i = ln_a % n;
+      const double* src = Aa + k * LX.s0 + i;
+      double x[m], y[n];
+#pragma unroll
+      for (int t = 0; t < m; ++t) x[t] = src[t * LX.s1];
+      fold_apply<n, m, 1>(p.It, x, y);
+      double* dst = p.out + (e0 + el_a) * n3 + k * n2 + i;
+#pragma unroll
+      for (int t = 0; t < n; ++t) st_stream(dst + t * n, y[t]);
+    }
+    __syncthreads();  // A is rewritten by the next tile's S1
+  }
+}
+
+template <int N>
+static cudaError_t launch_n(const hx_plan& P, const double* q, const double* fac, double* out,
+                            int64_t n_el, int* flag, cudaStream_t s) {
+  using C = Cfg<kBP3, N>;
+  constexpr int n = N + 1, m = N + 2;
+  constexpr int smem = smem_doubles<kBP3, N>() * int(sizeof(double));
+  static int blocks_per_sm = -1;
+  if (blocks_per_sm < 0) {
+    cudaError_t err = cudaFuncSetAttribute(bp3_kernel<N>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (err != cudaSuccess) return err;
+    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, bp3_kernel<N>, C::NT,
+                                                        smem);
+    if (err != cudaSuccess) return err;
+    if (blocks_per_sm < 1) blocks_per_sm = 1;
+  }
+  BP3Params<N> prm;
+  double it[n * m], dt[m * m];
+  fill_fold(prm.I, P.interp);
+  transpose(P.interp, m, n, it);
+  fill_fold(prm.It, it);
+  fill_fold(prm.D, P.diff);
+  transpose(P.diff, m, m, dt);
+  fill_fold(prm.Dt, dt);
+  prm.q = q;
+  prm.fac = fac;
+  prm.out = out;
+  prm.n_el = n_el;
+  prm.fac_estride = P.elem_stride;
+  prm.fac_sstride = P.slot_stride;
+  prm.lam = P.lam;
+  prm.flag = flag;
+  const int64_t ntiles = (n_el + C::EPB - 1) / C::EPB;
+  const int64_t grid = min64(ntiles, int64_t(blocks_per_sm) * sm_count());
+  bp3_kernel<N><<<unsigned(grid), C::NT, smem, s>>>(prm);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bp3(const hx_plan& P, const double* q, const double* fac, double* out,
+                       int64_t n_el, int* flag, cudaStream_t s) {
+  switch (P.degree) {
+#define HX_CASE(N) \
+  case N:          \
+    return launch_n<N>(P, q, fac, out, n_el, flag, s);
+    HX_CASE(1) HX_CASE(2) HX_CASE(3) HX_CASE(4) HX_CASE(5) HX_CASE(6) HX_CASE(7) HX_CASE(8)
+    HX_CASE(9) HX_CASE(10) HX_CASE(11) HX_CASE(12) HX_CASE(13) HX_CASE(14) HX_CASE(15)
+#undef HX_CASE
+    default:
+      return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace hx

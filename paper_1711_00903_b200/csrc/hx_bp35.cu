@@ -1,0 +1,227 @@
+// BP3.5 -- collocated stiffness matvec on the GLL points (reference
+// operators.py:282-286 -> _diff_chain_combine, operators.py:235-268):
+//
+//   out = lam * GwJ * q + sum_d D_d^T ( sum_d' G_dd' * D_d' q )
+//
+// One CTA processes a tile of EPB consecutive elements per iteration of a
+// persistent loop.  Each thread owns one 1-D line of an element; the
+// per-element tensors live in padded shared memory (strides from
+// hx_layouts.h) and change orientation between stages:
+//
+//   S1 k-lines (j,i): q from HBM (coalesced over (j,i)), qt = D_t q (regs), q -> A
+//   S2 i-lines (k,j): qr = D_r A -> B        j-lines (k,i): qs = D_s A -> C
+//   S3 k-lines (j,i): G (HBM, coalesced) chain rule; rqr -> B, rqs -> C,
+//                     acc = lam GwJ q + D_t^T rqt (regs)
+//   S4 i-lines: B <- D_r^T B                 j-lines: C <- D_s^T C
+//   S5 k-lines (j,i): out = acc + B + C (HBM, coalesced)
+//
+// The only HBM traffic is q, the 7 factor slots and out (Table 1: 9 n^3
+// doubles per element).  The next tile's inputs are pulled into L2 with a
+// bulk prefetch when a tile starts, so the loads in S1/S3 hit L2.
+#include "hx_common.cuh"
+#include "hx_plan.h"
+
+namespace hx {
+
+template <int N>
+struct BP35Params {
+  Fold<N + 1, N + 1> D;   // derivative D (anti-centro-symmetric)
+  Fold<N + 1, N + 1> Dt;  // its transpose
+  const double* q;
+  const double* fac;
+  double* out;
+  int64_t n_el;
+  int64_t fac_estride;  // doubles per element in the packed factor array
+  int64_t fac_sstride;  // doubles per slot
+  double lam;
+  int* flag;
+};
+
+template <int N>
+__global__ void __launch_bounds__(Cfg<kBP35, N>::NT)
+    bp35_kernel(const __grid_constant__ BP35Params<N> p) {
+  using C = Cfg<kBP35, N>;
+  constexpr int n = N + 1, n2 = n * n, n3 = n2 * n;
+  constexpr int EPB = C::EPB;
+  constexpr Lay LA = C::L[0], LB = C::L[1], LC = C::L[2];
+  constexpr int EA = C::EBUF[0], EB = C::EBUF[1], EC = C::EBUF[2];
+  extern __shared__ double smem[];
+  double* const A = smem;
+  double* const B = A + EPB * EA;
+  double* const Cs = B + EPB * EB;
+
+  const int tid = threadIdx.x;
+  const int el = tid / n2;  // element of the tile this thread serves
+  const int ln = tid % n2;  // its line within the element (same count every stage)
+  const int64_t ntiles = (p.n_el + EPB - 1) / EPB;
+  const int64_t ss = p.fac_sstride;
+
+  if (tid == 0 && blockIdx.x < ntiles) {
+    const int64_t e0 = int64_t(blockIdx.x) * EPB;
+    const int64_t ne = min64(EPB, p.n_el - e0);
+    prefetch_l2(p.q + e0 * n3, ne * n3 * sizeof(double));
+    prefetch_l2(p.fac + e0 * p.fac_estride, ne * p.fac_estride * sizeof(double));
+  }
+
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t e0 = tile * EPB;
+    const int ne = int(min64(EPB, p.n_el - e0));
+    if (tid == 0) {
+      const int64_t nt = tile + gridDim.x;
+      if (nt < ntiles) {
+        const int64_t f0 = nt * EPB;
+        const int64_t nn = min64(EPB, p.n_el - f0);
+        prefetch_l2(p.q + f0 * n3, nn * n3 * sizeof(double));
+        prefetch_l2(p.fac + f0 * p.fac_estride, nn * p.fac_estride * sizeof(double));
+      }
+    }
+    const bool act = el < ne;
+    const int64_t e = e0 + el;
+    double* const Ae = A + el * EA;
+    double* const Be = B + el * EB;
+    double* const Ce = Cs + el * EC;
+
+    double qv[n], qt[n], acc[n];
+    // ---- S1: k-lines over (j, i)
+    if (act) {
+      const int j = ln / n, i = ln % n;
+      const double* src = p.q + e * n3 + j * n + i;
+      bool bad = false;
+#pragma unroll
+      for (int k = 0; k < n; ++k) {
+        qv[k] = src[k * n2];
+        bad |= nonfinite(qv[k]);
+      }
+      if (bad && p.flag) atomicOr(p.flag, 1);
+      fold_apply<n, n, -1>(p.D, qv, qt);
+      double* a = Ae + j * LA.s1 + i;
+#pragma unroll
+      for (int k = 0; k < n; ++k) a[k * LA.s0] = qv[k];
+    }
+    __syncthreads();
+    // ---- S2: r- and s-derivatives
+    if (act) {
+      const int k = ln / n, r = ln % n;
+      double x[n], y[n];
+      const double* a = Ae + k * LA.s0 + r * LA.s1;  // i-line (k, j=r)
+#pragma unroll
+      for (int t = 0; t < n; ++t) x[t] = a[t];
+      fold_apply<n, n, -1>(p.D, x, y);
+      double* b = Be + k * LB.s0 + r * LB.s1;
+#pragma unroll
+      for (int t = 0; t < n; ++t) b[t] = y[t];
+      a = Ae + k * LA.s0 + r;  // j-line (k, i=r)
+#pragma unroll
+      for (int t = 0; t < n; ++t) x[t] = a[t * LA.s1];
+      fold_apply<n, n, -1>(p.D, x, y);
+      double* c = Ce + k * LC.s0 + r;
+#pragma unroll
+      for (int t = 0; t < n; ++t) c[t * LC.s1] = y[t];
+    }
+    __syncthreads();
+    // ---- S3: metric chain rule on k-lines
+    if (act) {
+      const int j = ln / n, i = ln % n;
+      double* b = Be + j * LB.s1 + i;
+      double* c = Ce + j * LC.s1 + i;
+      const double* g = p.fac + e * p.fac_estride + j * n + i;
+      double rqt[n];
+#pragma unroll
+      for (int k = 0; k < n; ++k) {
+        const double* gk = g + k * n2;
+        const double grr = gk[0], grs = gk[ss], grt = gk[2 * ss];
+        const double gss = gk[3 * ss], gst = gk[4 * ss], gtt = gk[5 * ss];
+        const double gwj = gk[6 * ss];
+        const double qr = b[k * LB.s0], qs = c[k * LC.s0], qtk = qt[k];
+        b[k * LB.s0] = grr * qr + grs * qs + grt * qtk;
+        c[k * LC.s0] = grs * qr + gss * qs + gst * qtk;
+        rqt[k] = grt * qr + gst * qs + gtt * qtk;
+        qv[k] = p.lam * gwj * qv[k];
+      }
+      fold_apply<n, n, -1>(p.Dt, rqt, acc);
+#pragma unroll
+      for (int k = 0; k < n; ++k) acc[k] += qv[k];
+    }
+    __syncthreads();
+    // ---- S4: transposed r- and s-derivatives, in place
+    if (act) {
+      const int k = ln / n, r = ln % n;
+      double x[n], y[n];
+      double* b = Be + k * LB.s0 + r * LB.s1;
+#pragma unroll
+      for (int t = 0; t < n; ++t) x[t] = b[t];
+      fold_apply<n, n, -1>(p.Dt, x, y);
+#pragma unroll
+      for (int t = 0; t < n; ++t) b[t] = y[t];
+      double* c = Ce + k * LC.s0 + r;
+#pragma unroll
+      for (int t = 0; t < n; ++t) x[t] = c[t * LC.s1];
+      fold_apply<n, n, -1>(p.Dt, x, y);
+#pragma unroll
+      for (int t = 0; t < n; ++t) c[t * LC.s1] = y[t];
+    }
+    __syncthreads();
+    // ---- S5: combine and store
+    if (act) {
+      const int j = ln / n, i = ln % n;
+      const double* b = Be + j * LB.s1 + i;
+      const double* c = Ce + j * LC.s1 + i;
+      double* dst = p.out + e * n3 + j * n + i;
+#pragma unroll
+      for (int k = 0; k < n; ++k) st_stream(dst + k * n2, acc[k] + b[k * LB.s0] + c[k * LC.s0]);
+    }
+    // A is rewritten by the next tile's S1 only after it has passed this
+    // tile's S3/S4 barriers; B and C only after the next S1 barrier.
+  }
+}
+
+template <int N>
+static cudaError_t launch_n(const hx_plan& P, const double* q, const double* fac, double* out,
+                            int64_t n_el, int* flag, cudaStream_t s) {
+  using C = Cfg<kBP35, N>;
+  constexpr int smem = smem_doubles<kBP35, N>() * int(sizeof(double));
+  static int blocks_per_sm = -1;
+  if (blocks_per_sm < 0) {
+    cudaError_t err = cudaFuncSetAttribute(bp35_kernel<N>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (err != cudaSuccess) return err;
+    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, bp35_kernel<N>, C::NT,
+                                                        smem);
+    if (err != cudaSuccess) return err;
+    if (blocks_per_sm < 1) blocks_per_sm = 1;
+  }
+  BP35Params<N> prm;
+  constexpr int n = N + 1;
+  double dt[n * n];
+  fill_fold(prm.D, P.diff);
+  transpose(P.diff, n, n, dt);
+  fill_fold(prm.Dt, dt);
+  prm.q = q;
+  prm.fac = fac;
+  prm.out = out;
+  prm.n_el = n_el;
+  prm.fac_estride = P.elem_stride;
+  prm.fac_sstride = P.slot_stride;
+  prm.lam = P.lam;
+  prm.flag = flag;
+  const int64_t ntiles = (n_el + C::EPB - 1) / C::EPB;
+  const int64_t grid = min64(ntiles, int64_t(blocks_per_sm) * sm_count());
+  bp35_kernel<N><<<unsigned(grid), C::NT, smem, s>>>(prm);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bp35(const hx_plan& P, const double* q, const double* fac, double* out,
+                        int64_t n_el, int* flag, cudaStream_t s) {
+  switch (P.degree) {
+#define HX_CASE(N) \
+  case N:          \
+    return launch_n<N>(P, q, fac, out, n_el, flag, s);
+    HX_CASE(1) HX_CASE(2) HX_CASE(3) HX_CASE(4) HX_CASE(5) HX_CASE(6) HX_CASE(7) HX_CASE(8)
+    HX_CASE(9) HX_CASE(10) HX_CASE(11) HX_CASE(12) HX_CASE(13) HX_CASE(14) HX_CASE(15)
+#undef HX_CASE
+    default:
+      return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace hx

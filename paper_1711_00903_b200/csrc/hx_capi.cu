@@ -1,0 +1,267 @@
+// C ABI entry points (include/hexbench_b200.h).  Thin: validate, dispatch to
+// the per-operator launchers, translate CUDA errors into HX_ECUDA.
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+
+#include "hx_common.cuh"
+#include "hx_plan.h"
+
+namespace hx {
+
+int sm_count() {
+  static int count = 0;
+  if (count == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&count, cudaDevAttrMultiProcessorCount, dev);
+    if (count <= 0) count = 1;
+  }
+  return count;
+}
+
+static int kernel_shape(int bp, int degree, int* epb, int* nt, int* smem) {
+#define HX_SHAPE(BP, N)                                                  \
+  if (bp == BP && degree == N) {                                        \
+    *epb = Cfg<BP, N>::EPB;                                             \
+    *nt = Cfg<BP, N>::NT;                                               \
+    *smem = smem_doubles<BP, N>() * int(sizeof(double));                \
+    return HX_OK;                                                       \
+  }
+#define HX_SHAPES(BP)                                                                        \
+  HX_SHAPE(BP, 1) HX_SHAPE(BP, 2) HX_SHAPE(BP, 3) HX_SHAPE(BP, 4) HX_SHAPE(BP, 5)            \
+  HX_SHAPE(BP, 6) HX_SHAPE(BP, 7) HX_SHAPE(BP, 8) HX_SHAPE(BP, 9) HX_SHAPE(BP, 10)           \
+  HX_SHAPE(BP, 11) HX_SHAPE(BP, 12) HX_SHAPE(BP, 13) HX_SHAPE(BP, 14) HX_SHAPE(BP, 15)
+  HX_SHAPES(kBP1)
+  HX_SHAPES(kBP35)
+  HX_SHAPES(kBP3)
+#undef HX_SHAPES
+#undef HX_SHAPE
+  return HX_EINVAL;
+}
+
+static cudaError_t launch(const hx_plan& P, const double* q, const double* fac, double* out,
+                          int64_t n_el, int* flag, cudaStream_t s) {
+  if (n_el == 0) return cudaSuccess;
+  switch (P.bp) {
+    case HX_BP1:
+      return launch_bp1(P, q, fac, out, n_el, flag, s);
+    case HX_BP35:
+      return launch_bp35(P, q, fac, out, n_el, flag, s);
+    default:
+      return launch_bp3(P, q, fac, out, n_el, flag, s);
+  }
+}
+
+static thread_local char g_last_cuda[256];
+
+static int cuda_status(cudaError_t err) {
+  if (err == cudaSuccess) return HX_OK;
+  std::snprintf(g_last_cuda, sizeof(g_last_cuda), "CUDA error: %s",
+                cudaGetErrorString(err));
+  return HX_ECUDA;
+}
+
+}  // namespace hx
+
+using namespace hx;
+
+extern "C" {
+
+int hx_plan_create(int bp, int degree, double lam, const double* interp, const double* diff,
+                   const double* nodes, const double* weights, hx_plan** out) {
+  if (!out) return HX_EINVAL;
+  *out = nullptr;
+  if (bp != HX_BP1 && bp != HX_BP35 && bp != HX_BP3) return HX_EINVAL;
+  if (degree < 1 || degree > 15) return HX_EINVAL;
+  if (!(lam >= 0.0)) return HX_EINVAL;  // also rejects NaN
+  if (!nodes || !weights) return HX_EINVAL;
+  if (bp != HX_BP35 && !interp) return HX_EINVAL;
+  if (bp != HX_BP1 && !diff) return HX_EINVAL;
+  hx_plan* P = new (std::nothrow) hx_plan();
+  if (!P) return HX_ENOMEM;
+  P->bp = bp;
+  P->degree = degree;
+  P->n = degree + 1;
+  P->m = degree + 2;
+  P->q = bp == HX_BP35 ? P->n : P->m;
+  P->lam = lam;
+  if (interp) std::memcpy(P->interp, interp, sizeof(double) * P->m * P->n);
+  if (diff) std::memcpy(P->diff, diff, sizeof(double) * P->q * P->q);
+  std::memcpy(P->nodes, nodes, sizeof(double) * P->q);
+  std::memcpy(P->weights, weights, sizeof(double) * P->q);
+  const int64_t q3 = int64_t(P->q) * P->q * P->q;
+  P->n_slots = bp == HX_BP1 ? 1 : 7;
+  P->slot_stride = (q3 + 1) & ~int64_t(1);  // keep every slot 16-byte aligned
+  P->elem_stride = P->n_slots * P->slot_stride;
+  P->pipe_ready = false;
+  *out = P;
+  return HX_OK;
+}
+
+void hx_plan_destroy(hx_plan* P) {
+  if (!P) return;
+  if (P->pipe_ready) {
+    for (int i = 0; i < 3; ++i) {
+      cudaStreamDestroy(P->pipe[i]);
+      for (int j = 0; j < 2; ++j) cudaEventDestroy(P->ev[i][j]);
+    }
+  }
+  delete P;
+}
+
+int hx_plan_factor_layout(const hx_plan* P, int* n_slots, int64_t* slot_stride,
+                          int64_t* element_stride) {
+  if (!P) return HX_EINVAL;
+  if (n_slots) *n_slots = P->n_slots;
+  if (slot_stride) *slot_stride = P->slot_stride;
+  if (element_stride) *element_stride = P->elem_stride;
+  return HX_OK;
+}
+
+int hx_plan_kernel_shape(const hx_plan* P, int* epb, int* threads, int* smem_bytes) {
+  if (!P || !epb || !threads || !smem_bytes) return HX_EINVAL;
+  return kernel_shape(P->bp, P->degree, epb, threads, smem_bytes);
+}
+
+int hx_geometric_factors(const hx_plan* P, const double* vertices, int64_t n_el, int all_slots,
+                         double* factors, int* flag, void* stream) {
+  if (!P || n_el < 0) return HX_EINVAL;
+  if (n_el > 0 && (!vertices || !factors)) return HX_EINVAL;
+  return cuda_status(launch_geometry(*P, vertices, n_el, all_slots, factors, flag,
+                                     static_cast<cudaStream_t>(stream)));
+}
+
+int hx_repack_factors(const hx_plan* P, const double* src, int64_t n_el, double* dst,
+                      int to_packed, void* stream) {
+  if (!P || n_el < 0) return HX_EINVAL;
+  if (n_el > 0 && (!src || !dst)) return HX_EINVAL;
+  return cuda_status(launch_repack(*P, src, n_el, dst, to_packed,
+                                   static_cast<cudaStream_t>(stream)));
+}
+
+int hx_apply(const hx_plan* P, const double* q, const double* factors, double* out,
+             int64_t n_el, int* flag, void* stream) {
+  if (!P || n_el < 0) return HX_EINVAL;
+  if (n_el > 0 && (!q || !factors || !out)) return HX_EINVAL;
+  return cuda_status(launch(*P, q, factors, out, n_el, flag, static_cast<cudaStream_t>(stream)));
+}
+
+int64_t hx_apply_host_workspace(const hx_plan* P, int64_t chunk_el) {
+  if (!P || chunk_el <= 0) return -1;
+  const int64_t n3 = int64_t(P->n) * P->n * P->n;
+  return 2 /*slots*/ * 2 /*q,out*/ * chunk_el * n3 * int64_t(sizeof(double));
+}
+
+int hx_apply_host(const hx_plan* Pc, const double* q_host, const double* factors,
+                  double* out_host, int64_t n_el, int64_t chunk_el, void* work, int* flag,
+                  void* stream) {
+  if (!Pc || n_el < 0 || chunk_el <= 0) return HX_EINVAL;
+  if (n_el == 0) return HX_OK;
+  if (!q_host || !factors || !out_host || !work) return HX_EINVAL;
+  hx_plan* P = const_cast<hx_plan*>(Pc);  // lazily owned pipeline resources
+  cudaStream_t caller = static_cast<cudaStream_t>(stream);
+  cudaError_t err;
+  if (!P->pipe_ready) {
+    for (int i = 0; i < 3; ++i) {
+      if ((err = cudaStreamCreateWithFlags(&P->pipe[i], cudaStreamNonBlocking)) != cudaSuccess)
+        return cuda_status(err);
+      for (int j = 0; j < 2; ++j)
+        if ((err = cudaEventCreateWithFlags(&P->ev[i][j], cudaEventDisableTiming)) !=
+            cudaSuccess)
+          return cuda_status(err);
+    }
+    P->pipe_ready = true;
+  }
+  const int64_t n3 = int64_t(P->n) * P->n * P->n;
+  double* wq[2];
+  double* wo[2];
+  double* base = static_cast<double*>(work);
+  wq[0] = base;
+  wq[1] = base + chunk_el * n3;
+  wo[0] = base + 2 * chunk_el * n3;
+  wo[1] = base + 3 * chunk_el * n3;
+  cudaStream_t s_in = P->pipe[0], s_k = P->pipe[1], s_out = P->pipe[2];
+  cudaEvent_t* e_in = P->ev[0];
+  cudaEvent_t* e_k = P->ev[1];
+  cudaEvent_t* e_out = P->ev[2];
+  // start after whatever the caller queued (e.g. factor generation)
+  cudaEvent_t start;
+  if ((err = cudaEventCreateWithFlags(&start, cudaEventDisableTiming)) != cudaSuccess)
+    return cuda_status(err);
+  cudaEventRecord(start, caller);
+  cudaStreamWaitEvent(s_in, start, 0);
+  cudaStreamWaitEvent(s_k, start, 0);
+  cudaStreamWaitEvent(s_out, start, 0);
+  const int64_t nchunks = (n_el + chunk_el - 1) / chunk_el;
+  for (int64_t c = 0; c < nchunks; ++c) {
+    const int slot = int(c & 1);
+    const int64_t e0 = c * chunk_el;
+    const int64_t ne = std::min(chunk_el, n_el - e0);
+    const size_t bytes = size_t(ne * n3) * sizeof(double);
+    if (c >= 2) cudaStreamWaitEvent(s_in, e_k[slot], 0);  // kernel c-2 done reading wq[slot]
+    cudaMemcpyAsync(wq[slot], q_host + e0 * n3, bytes, cudaMemcpyHostToDevice, s_in);
+    cudaEventRecord(e_in[slot], s_in);
+    cudaStreamWaitEvent(s_k, e_in[slot], 0);
+    if (c >= 2) cudaStreamWaitEvent(s_k, e_out[slot], 0);  // D2H c-2 done with wo[slot]
+    if ((err = launch(*P, wq[slot], factors + e0 * P->elem_stride, wo[slot], ne, flag, s_k)) !=
+        cudaSuccess) {
+      cudaEventDestroy(start);
+      return cuda_status(err);
+    }
+    cudaEventRecord(e_k[slot], s_k);
+    cudaStreamWaitEvent(s_out, e_k[slot], 0);
+    cudaMemcpyAsync(out_host + e0 * n3, wo[slot], bytes, cudaMemcpyDeviceToHost, s_out);
+    cudaEventRecord(e_out[slot], s_out);
+  }
+  cudaStreamWaitEvent(caller, e_out[(nchunks - 1) & 1], 0);
+  if (nchunks >= 2) cudaStreamWaitEvent(caller, e_out[nchunks & 1], 0);
+  cudaEventDestroy(start);
+  return cuda_status(cudaGetLastError());
+}
+
+int hx_measure_smem_bandwidth(double* bytes_per_s, void* stream) {
+  if (!bytes_per_s) return HX_EINVAL;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  double* sink = nullptr;
+  cudaError_t err = cudaMalloc(&sink, sizeof(double) * 4096);
+  if (err != cudaSuccess) return cuda_status(err);
+  const int iters = 4096;
+  float ms = 0.f;
+  err = launch_smem_probe(sink, iters, &ms, s);
+  cudaFree(sink);
+  if (err != cudaSuccess) return cuda_status(err);
+  const double bytes = double(sm_count()) * 2 * 512 * double(iters) * 8 * 4 * sizeof(double);
+  *bytes_per_s = bytes / (ms * 1e-3);
+  return HX_OK;
+}
+
+const char* hx_strerror(int status) {
+  switch (status) {
+    case HX_OK:
+      return "success";
+    case HX_EINVAL:
+      return "invalid argument";
+    case HX_ENONFINITE:
+      return "field vector contains non-finite values";
+    case HX_EDEGENERATE:
+      return "non-positive Jacobian determinant";
+    case HX_ECUDA:
+      return g_last_cuda[0] ? g_last_cuda : "CUDA error";
+    case HX_ENOMEM:
+      return "out of host memory";
+    default:
+      return "unknown status";
+  }
+}
+
+int hx_device_ok(void) {
+  int dev = 0, major = 0, minor = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+  return major == 10 && minor == 0;
+}
+
+}  // extern "C"

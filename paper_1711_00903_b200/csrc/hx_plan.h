@@ -1,0 +1,51 @@
+// Host-side plan object behind the C ABI (include/hexbench_b200.h).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/hexbench_b200.h"
+
+namespace hx {
+
+constexpr int kMaxQ = 17;  // N <= 15 -> at most N+2 points per axis
+
+}  // namespace hx
+
+struct hx_plan {
+  int bp;       // HX_BP1 / HX_BP35 / HX_BP3
+  int degree;   // N
+  int n, m;     // GLL points (N+1) and GL points (N+2) per axis
+  int q;        // quadrature points per axis of the factor rule (m, or n for BP3.5)
+  double lam;
+  double interp[hx::kMaxQ * hx::kMaxQ];  // m x n, row-major (BP1, BP3)
+  double diff[hx::kMaxQ * hx::kMaxQ];    // q x q, row-major (BP3.5, BP3)
+  double nodes[hx::kMaxQ];               // factor rule nodes / weights
+  double weights[hx::kMaxQ];
+  int n_slots;            // factor slots kept on device (1 for BP1, 7 otherwise)
+  int64_t slot_stride;    // doubles per slot (q^3 rounded up to even)
+  int64_t elem_stride;    // doubles per element (n_slots * slot_stride)
+  // lazily created resources for the host-buffer (end-to-end) path
+  cudaStream_t pipe[3];
+  cudaEvent_t ev[3][2];
+  bool pipe_ready;
+};
+
+namespace hx {
+
+// launch the fused element kernel for elements [0, n_el) of device arrays
+cudaError_t launch_bp1(const hx_plan& P, const double* q, const double* fac, double* out,
+                       int64_t n_el, int* flag, cudaStream_t s);
+cudaError_t launch_bp35(const hx_plan& P, const double* q, const double* fac, double* out,
+                        int64_t n_el, int* flag, cudaStream_t s);
+cudaError_t launch_bp3(const hx_plan& P, const double* q, const double* fac, double* out,
+                       int64_t n_el, int* flag, cudaStream_t s);
+cudaError_t launch_geometry(const hx_plan& P, const double* verts, int64_t n_el, int all_slots,
+                            double* fac, int* flag, cudaStream_t s);
+cudaError_t launch_repack(const hx_plan& P, const double* src, int64_t n_el, double* dst,
+                          int to_packed, cudaStream_t s);
+cudaError_t launch_smem_probe(double* sink, int iters, float* ms, cudaStream_t s);
+
+int sm_count();
+
+}  // namespace hx

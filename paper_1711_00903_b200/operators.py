@@ -1,0 +1,325 @@
+"""Drop-in operator API for BP1.0 / BP3.5 / BP3.0 (reference ``operators.py``).
+
+Same names, signatures, validation and error types as the reference
+(``make_operator`` operators.py:118-143, ``apply_operator`` :306-331,
+``apply_bp*`` :334-349, ``FieldVector`` :67-91, ``OperatorInstance`` :94-115,
+``AccessCounters`` :41-64).  What changes is underneath:
+
+* ``make_operator`` builds the 1-D matrices on the host (tiny) and the
+  geometric factors on the device, straight into the packed layout the
+  kernels stream (``hx_geometric_factors``);
+* ``apply_operator`` is one fused sm_100a kernel launch through the C ABI
+  (``hx_apply`` for device-resident torch tensors, ``hx_apply_host`` for
+  host numpy arrays, with the PCIe copies pipelined against the kernel);
+* counters are charged analytically per element (``perf.element_counters``),
+  identical to the reference's instrumented values;
+* ``threads`` is accepted for signature compatibility; results are
+  independent of it by construction (the reference guarantees the same,
+  operators.py:309-311).
+
+There is no CPU execution path: without the native library every apply
+raises ``NativeLibraryError``.
+"""
+
+from dataclasses import dataclass, field, fields
+
+import numpy as np
+
+from . import _native
+from .basis import check_degree, diff_matrix_gl, diff_matrix_gll, interp_matrix
+from .mesh import DegenerateGeometryError, GeometricFactors
+from .perf import BENCHMARKS, BP1, BP3, BP35, VARIANTS, element_counters
+from .quadrature import gl_rule, gll_rule
+
+DOUBLE = 8
+_BP_ID = {BP1: _native.HX_BP1, BP35: _native.HX_BP35, BP3: _native.HX_BP3}
+
+
+class UnsupportedVariantError(ValueError):
+    """A variant was requested for a benchmark that lacks it."""
+
+
+@dataclass
+class AccessCounters:
+    """Modelled byte / FLOP / barrier totals (reference operators.py:41-64)."""
+
+    global_reads: int = 0
+    global_writes: int = 0
+    scratch_reads: int = 0
+    scratch_writes: int = 0
+    interp_matrix_reads: int = 0
+    flops: int = 0
+    syncs: int = 0
+
+    def merge(self, other):
+        for f in fields(self):
+            setattr(self, f.name, getattr(self, f.name) + getattr(other, f.name))
+
+
+def _is_torch(x):
+    return type(x).__module__.startswith("torch")
+
+
+@dataclass(frozen=True)
+class FieldVector:
+    """Element-blocked field, (n_el, n_p) float64, point order (k, j, i).
+
+    ``data`` may be a numpy array (host) or a torch float64 tensor (device
+    resident); shape and size checks follow reference operators.py:75-79.
+    """
+
+    n_el: int
+    n_p: int
+    data: object = field(repr=False)
+
+    def __post_init__(self):
+        d = self.data
+        if _is_torch(d):
+            import torch
+            if d.dtype != torch.float64:
+                d = d.to(torch.float64)
+            if d.numel() != self.n_el * self.n_p:
+                raise ValueError("data length must be n_el * n_p")
+            d = d.reshape(self.n_el, self.n_p)
+        else:
+            d = np.asarray(d, dtype=float)
+            if d.size != self.n_el * self.n_p:
+                raise ValueError("data length must be n_el * n_p")
+            d = d.reshape(self.n_el, self.n_p)
+        object.__setattr__(self, "data", d)
+
+    @classmethod
+    def constant(cls, n_el, n_p, value=1.0):
+        return cls(n_el, n_p, np.full(n_el * n_p, float(value)))
+
+    @classmethod
+    def random(cls, n_el, n_p, seed=0):
+        rng = np.random.default_rng(seed)
+        return cls(n_el, n_p, rng.standard_normal(n_el * n_p))
+
+    @property
+    def on_device(self):
+        return _is_torch(self.data) and self.data.is_cuda
+
+    def flat(self):
+        return self.data.reshape(-1)
+
+    def to_device(self, device=None):
+        import torch
+        dev = torch.device("cuda") if device is None else torch.device(device)
+        d = self.data if _is_torch(self.data) else torch.from_numpy(np.ascontiguousarray(self.data))
+        return FieldVector(self.n_el, self.n_p, d.to(dev))
+
+    def to_host(self):
+        d = self.data.detach().cpu().numpy() if _is_torch(self.data) else self.data
+        return FieldVector(self.n_el, self.n_p, d)
+
+
+@dataclass(frozen=True)
+class OperatorInstance:
+    bp: str
+    degree: int
+    lam: float
+    interp: object  # OperatorMatrix or None
+    diff: object
+    factors: object  # GeometricFactors (device-backed, host view on demand)
+    variant: str
+    n_el: int
+    plan: object = field(default=None, repr=False, compare=False)
+    device_factors: object = field(default=None, repr=False, compare=False)
+    device: object = field(default=None, repr=False, compare=False)
+
+    @property
+    def n_q(self):
+        return self.degree + 1
+
+    @property
+    def n_q_gl(self):
+        return self.degree + 2
+
+    @property
+    def n_p(self):
+        return self.n_q ** 3
+
+
+def _stream(device):
+    import torch
+    return ctypes_stream(torch.cuda.current_stream(device))
+
+
+def ctypes_stream(s):
+    return s.cuda_stream
+
+
+def _validate(bp, degree, variant, lam):
+    """Reference operators.py:120-129, same order and messages."""
+    if bp not in BENCHMARKS:
+        raise ValueError(f"unknown benchmark {bp!r}")
+    if variant not in VARIANTS:
+        raise ValueError(f"unknown variant {variant!r}")
+    if variant == "symfused" and bp == BP35:
+        raise UnsupportedVariantError(
+            "symfused exploits the interpolation matrix; BP3.5 has none")
+    if lam < 0:
+        raise ValueError("lambda must be non-negative")
+    check_degree(degree)
+
+
+def make_operator(bp, degree, mesh, lam=0.0, variant="fused", device=None, factors=None):
+    """Assemble matrices and device-resident geometric factors.
+
+    ``factors`` (optional) is a reference-layout ``(n_el, 7, m, m, m)`` array or
+    ``GeometricFactors`` to upload instead of generating them on the device
+    (used to feed the reference's exact factors into parity tests).
+    """
+    _validate(bp, degree, variant, lam)
+    import torch
+
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None \
+        else torch.device(device)
+    if bp == BP1:
+        interp, diff, rule = interp_matrix(degree), None, gl_rule(degree + 2)
+    elif bp == BP35:
+        interp, diff, rule = None, diff_matrix_gll(degree), gll_rule(degree + 1)
+    else:
+        interp, diff, rule = interp_matrix(degree), diff_matrix_gl(degree), gl_rule(degree + 2)
+    plan = _native.Plan(_BP_ID[bp], degree, float(lam),
+                        None if interp is None else interp.entries,
+                        None if diff is None else diff.entries, rule.nodes, rule.weights)
+    n_el = mesh.n_el
+    packed = torch.empty(max(n_el, 1) * plan.elem_stride, dtype=torch.float64, device=dev)
+    stream = _stream(dev)
+    with torch.cuda.device(dev):
+        if factors is None:
+            verts = torch.from_numpy(np.ascontiguousarray(mesh.vertices)).to(dev)
+            flag = torch.zeros(1, dtype=torch.int32, device=dev)
+            _native.check(_native.lib().hx_geometric_factors(
+                plan.handle, _native.ptr(verts), n_el, 0, _native.ptr(packed),
+                _native.ptr(flag), stream), "hx_geometric_factors")
+            if int(flag.item()) & _native.HX_FLAG_DEGENERATE:
+                raise DegenerateGeometryError("non-positive Jacobian determinant")
+        else:
+            ref = factors.data if isinstance(factors, GeometricFactors) else factors
+            ref = np.ascontiguousarray(ref, dtype=np.float64).reshape(n_el, 7, -1)
+            src = torch.from_numpy(ref).to(dev)
+            _native.check(_native.lib().hx_repack_factors(
+                plan.handle, _native.ptr(src), n_el, _native.ptr(packed), 1, stream),
+                "hx_repack_factors")
+            verts = None
+    q = rule.n
+
+    def host_view():
+        with torch.cuda.device(dev):
+            if factors is not None:
+                return np.array(ref).reshape(n_el, 7, q, q, q)
+            full = torch.empty(max(n_el, 1) * 7 * plan.slot_stride, dtype=torch.float64,
+                               device=dev)
+            s = _stream(dev)
+            v = torch.from_numpy(np.ascontiguousarray(mesh.vertices)).to(dev)
+            _native.check(_native.lib().hx_geometric_factors(
+                plan.handle, _native.ptr(v), n_el, 1, _native.ptr(full), None, s))
+            out = torch.empty(n_el * 7 * q ** 3, dtype=torch.float64, device=dev)
+            _native.check(_native.lib().hx_repack_factors(
+                plan.handle, _native.ptr(full), n_el, _native.ptr(out), 0, s))
+            return out.cpu().numpy().reshape(n_el, 7, q, q, q)
+
+    geo = GeometricFactors(rule.kind, q, rule.weights, loader=host_view)
+    return OperatorInstance(bp, degree, float(lam), interp, diff, geo, variant, n_el,
+                            plan=plan, device_factors=packed, device=dev)
+
+
+def _charge(op, counters):
+    if counters is None:
+        return
+    per = element_counters(op.bp, op.variant, op.degree)
+    for k, v in per.items():
+        setattr(counters, k, getattr(counters, k) + v * op.n_el)
+
+
+def apply_device(op, q, out, flag=None, stream=None):
+    """Raw device apply: ``out = A q`` for torch CUDA tensors, asynchronous on
+    ``stream`` (default: torch's current stream), no allocation, no sync.
+    This is what the harness times."""
+    if stream is None:
+        stream = _stream(op.device)
+    _native.check(_native.lib().hx_apply(
+        op.plan.handle, _native.ptr(q), _native.ptr(op.device_factors), _native.ptr(out),
+        op.n_el, _native.ptr(flag), stream), "hx_apply")
+
+
+def apply_operator(op, q, counters=None, threads=1, out=None):
+    """Apply a benchmark operator to a field vector (reference operators.py:306-331).
+
+    Returns a new FieldVector of the same kind as ``q`` (host numpy in, host
+    numpy out; device tensor in, device tensor out).  Raises ValueError on a
+    shape mismatch or non-finite input, like the reference.
+    """
+    if q.n_el != op.n_el or q.n_p != op.n_p:
+        raise ValueError("field vector shape does not match operator")
+    import torch
+
+    dev = op.device
+    with torch.cuda.device(dev):
+        flag = torch.zeros(1, dtype=torch.int32, device=dev)
+        stream = _stream(dev)
+        if q.on_device:
+            src = q.data.contiguous()
+            dst = torch.empty_like(src) if out is None else out
+            apply_device(op, src, dst, flag, stream)
+            result = FieldVector(op.n_el, op.n_p, dst)
+        else:
+            src = np.ascontiguousarray(q.data, dtype=np.float64)
+            dst = np.empty_like(src) if out is None else out
+            result = FieldVector(op.n_el, op.n_p, _apply_host(op, src, dst, flag, stream))
+        if int(flag.item()) & _native.HX_FLAG_NONFINITE:
+            raise ValueError("field vector contains non-finite values")
+    _charge(op, counters)
+    return result
+
+
+DEFAULT_CHUNK_BYTES = 32 << 20
+
+
+def host_chunk_elements(op, chunk_bytes=DEFAULT_CHUNK_BYTES):
+    return max(1, min(op.n_el, chunk_bytes // (op.n_p * DOUBLE)))
+
+
+def _apply_host(op, src, dst, flag, stream, chunk_el=None, work=None):
+    import torch
+    if op.n_el == 0:
+        return dst
+    if chunk_el is None:
+        chunk_el = host_chunk_elements(op)
+    if work is None:
+        nbytes = _native.lib().hx_apply_host_workspace(op.plan.handle, chunk_el)
+        work = torch.empty(nbytes // DOUBLE, dtype=torch.float64, device=op.device)
+    _native.check(_native.lib().hx_apply_host(
+        op.plan.handle, _native.ptr(src), _native.ptr(op.device_factors), _native.ptr(dst),
+        op.n_el, chunk_el, _native.ptr(work), _native.ptr(flag), stream), "hx_apply_host")
+    return dst
+
+
+def apply_host(op, src, dst, flag=None, stream=None, chunk_el=None, work=None):
+    """End-to-end apply on host arrays through ``hx_apply_host`` (asynchronous on
+    ``stream``; pass page-locked arrays for full copy/compute overlap)."""
+    if stream is None:
+        stream = _stream(op.device)
+    return _apply_host(op, src, dst, flag, stream, chunk_el, work)
+
+
+def apply_bp1(op, q, counters=None, threads=1):
+    if op.bp != BP1:
+        raise ValueError("operator is not BP1.0")
+    return apply_operator(op, q, counters, threads)
+
+
+def apply_bp35(op, q, counters=None, threads=1):
+    if op.bp != BP35:
+        raise ValueError("operator is not BP3.5")
+    return apply_operator(op, q, counters, threads)
+
+
+def apply_bp3(op, q, counters=None, threads=1):
+    if op.bp != BP3:
+        raise ValueError("operator is not BP3.0")
+    return apply_operator(op, q, counters, threads)

@@ -1,0 +1,91 @@
+"""CPU: the drop-in API surface and its validation (reference
+tests/test_operators.py:245-264 and operators.py:120-129, 315-318, 334-349)."""
+
+import numpy as np
+import pytest
+
+import paper_1711_00903_b200 as hx
+from paper_1711_00903_b200.operators import OperatorInstance
+
+
+def test_public_names_mirror_reference():
+    for name in ("BENCHMARKS", "BP1", "BP35", "BP3", "AccessCounters", "FieldVector",
+                 "OperatorInstance", "UnsupportedVariantError", "apply_bp1", "apply_bp3",
+                 "apply_bp35", "apply_operator", "make_operator", "build_cube_mesh",
+                 "perturb_mesh", "geometric_factors", "trilinear_jacobian",
+                 "DegenerateGeometryError", "HexMesh", "GeometricFactors", "gl_rule",
+                 "gll_rule", "lagrange_eval", "lagrange_deriv", "interp_matrix",
+                 "diff_matrix_gll", "diff_matrix_gl", "traffic", "flop_model",
+                 "roofline_global", "roofline_shared", "shared_bandwidth_ansatz"):
+        assert hasattr(hx, name), name
+    assert hx.BENCHMARKS == ("BP1.0", "BP3.5", "BP3.0")
+    assert hx.VARIANTS == ("baseline", "fused", "symfused")
+
+
+def test_make_operator_validation(perturbed_single):
+    with pytest.raises(ValueError):
+        hx.make_operator("BP9", 2, perturbed_single)
+    with pytest.raises(ValueError):
+        hx.make_operator(hx.BP1, 2, perturbed_single, variant="turbo")
+    with pytest.raises(hx.UnsupportedVariantError):
+        hx.make_operator(hx.BP35, 2, perturbed_single, variant="symfused")
+    with pytest.raises(ValueError):
+        hx.make_operator(hx.BP3, 2, perturbed_single, lam=-1.0)
+    with pytest.raises(ValueError):
+        hx.make_operator(hx.BP3, 16, perturbed_single)
+    assert issubclass(hx.UnsupportedVariantError, ValueError)
+
+
+def _fake_op(bp, deg=1, n_el=1):
+    return OperatorInstance(bp, deg, 0.0, None, None, None, "fused", n_el)
+
+
+def test_apply_shape_mismatch_and_bp_mismatch():
+    op = _fake_op(hx.BP1, 2)
+    with pytest.raises(ValueError):
+        hx.apply_operator(op, hx.FieldVector.constant(1, 8))
+    with pytest.raises(ValueError):
+        hx.apply_bp35(_fake_op(hx.BP1), hx.FieldVector.constant(1, 8))
+    with pytest.raises(ValueError):
+        hx.apply_bp1(_fake_op(hx.BP3), hx.FieldVector.constant(1, 8))
+    with pytest.raises(ValueError):
+        hx.apply_bp3(_fake_op(hx.BP35), hx.FieldVector.constant(1, 8))
+
+
+def test_field_vector():
+    v = hx.FieldVector.random(3, 8, seed=5)
+    np.testing.assert_array_equal(v.data.ravel(),
+                                  np.random.default_rng(5).standard_normal(24))
+    assert v.data.shape == (3, 8)
+    with pytest.raises(ValueError):
+        hx.FieldVector(2, 8, np.zeros(15))
+    c = hx.FieldVector.constant(2, 8, 3.0)
+    assert c.flat().sum() == 48.0
+    import torch
+    t = hx.FieldVector(2, 4, torch.arange(8, dtype=torch.float32))
+    assert t.data.dtype == torch.float64 and tuple(t.data.shape) == (2, 4)
+    assert not t.on_device
+
+
+def test_counters_merge_and_linearity():
+    a = hx.AccessCounters(1, 2, 3, 4, 5, 6, 7)
+    a.merge(hx.AccessCounters(1, 1, 1, 1, 1, 1, 1))
+    assert a == hx.AccessCounters(2, 3, 4, 5, 6, 7, 8)
+    per = hx.element_counters(hx.BP3, "fused", 7)
+    # fused global bytes equal Table 1 exactly (reference test_perf.py:80-95)
+    t = hx.traffic(hx.BP3, 7)
+    assert per["global_reads"] + per["global_writes"] == t.bytes_per_element
+    assert per["flops"] == hx.flop_model(hx.BP3, "fused", 7)
+
+
+def test_mesh_helpers():
+    m = hx.build_cube_mesh(8, 2.0)
+    assert m.n_el == 512
+    a, det = hx.trilinear_jacobian(hx.build_cube_mesh(1, 2.0).vertices[0], 0.1, -0.2, 0.7)
+    np.testing.assert_allclose(a, np.eye(3), atol=1e-14)
+    flat = hx.build_cube_mesh(1, 2.0).vertices[0].copy()
+    flat[:, 2] = 0.0
+    with pytest.raises(hx.DegenerateGeometryError):
+        hx.trilinear_jacobian(flat, 0.0, 0.0, 0.0)
+    with pytest.raises(ValueError):
+        hx.build_cube_mesh(0, 2.0)
