@@ -60,11 +60,12 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT)
   const int64_t ntiles = (p.n_el + EPB - 1) / EPB;
   const int64_t fs = p.fac_estride, ss = p.fac_sstride;
 
+  // L2 prefetch schedule (see hx_bp35.cu): a tile's factors are requested
+  // when S2 starts (consumed in S5), the next tile's q when S6 starts.
   if (tid == 0 && blockIdx.x < ntiles) {
     const int64_t e0 = int64_t(blockIdx.x) * EPB;
     const int64_t ne = min64(EPB, p.n_el - e0);
     prefetch_l2(p.q + e0 * n3, ne * n3 * sizeof(double));
-    prefetch_l2(p.fac + e0 * fs, ne * fs * sizeof(double));
   }
 
   const int el_a = tid / n2, ln_a = tid % n2;
@@ -74,15 +75,6 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT)
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t e0 = tile * EPB;
     const int ne = int(min64(EPB, p.n_el - e0));
-    if (tid == 0) {
-      const int64_t nt = tile + gridDim.x;
-      if (nt < ntiles) {
-        const int64_t f0 = nt * EPB;
-        const int64_t nn = min64(EPB, p.n_el - f0);
-        prefetch_l2(p.q + f0 * n3, nn * n3 * sizeof(double));
-        prefetch_l2(p.fac + f0 * fs, nn * fs * sizeof(double));
-      }
-    }
     double* const Aa = A + el_a * EA;
     double* const Ab = A + el_b * EA;
     double* const Ac = A + el_c * EA;
@@ -110,6 +102,7 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT)
     }
     __syncthreads();
     // ---- S2: i-lines (k, a): interpolate along r
+    if (tid == 0) prefetch_l2(p.fac + e0 * fs, ne * fs * sizeof(double));
     if (el_b < ne) {
       const int k = ln_b / m, a = ln_b % m;
       const double* src = Ab + k * LX.s0 + a * LX.s1;
@@ -182,6 +175,13 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT)
     }
     __syncthreads();
     // ---- S6: transposed r- and s-derivatives in place
+    if (tid == 0) {
+      const int64_t nt = tile + gridDim.x;
+      if (nt < ntiles) {
+        const int64_t f0 = nt * EPB;
+        prefetch_l2(p.q + f0 * n3, min64(EPB, p.n_el - f0) * n3 * sizeof(double));
+      }
+    }
     if (act_c) {
       const int kk = ln_c / m, r = ln_c % m;
       double x[m], y[m];

@@ -16,8 +16,8 @@
 //   S5 k-lines (j,i): out = acc + B + C (HBM, coalesced)
 //
 // The only HBM traffic is q, the 7 factor slots and out (Table 1: 9 n^3
-// doubles per element).  The next tile's inputs are pulled into L2 with a
-// bulk prefetch when a tile starts, so the loads in S1/S3 hit L2.
+// doubles per element).  Inputs are pulled into L2 ahead of use with bulk
+// prefetches (schedule below), so the loads in S1/S3 hit L2.
 #include "hx_common.cuh"
 #include "hx_plan.h"
 
@@ -56,25 +56,21 @@ __global__ void __launch_bounds__(Cfg<kBP35, N>::NT)
   const int64_t ntiles = (p.n_el + EPB - 1) / EPB;
   const int64_t ss = p.fac_sstride;
 
+  // L2 prefetch schedule.  The lead time must cover DRAM latency but stay
+  // short: prefetched-but-unconsumed bytes across all CTAs must fit in L2
+  // with room to spare, or lines are evicted and fetched twice.  So a
+  // tile's factors are requested when the tile starts (consumed in S3) and
+  // the next tile's q when S3 starts (consumed in the next S1).
   if (tid == 0 && blockIdx.x < ntiles) {
     const int64_t e0 = int64_t(blockIdx.x) * EPB;
     const int64_t ne = min64(EPB, p.n_el - e0);
     prefetch_l2(p.q + e0 * n3, ne * n3 * sizeof(double));
-    prefetch_l2(p.fac + e0 * p.fac_estride, ne * p.fac_estride * sizeof(double));
   }
 
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t e0 = tile * EPB;
     const int ne = int(min64(EPB, p.n_el - e0));
-    if (tid == 0) {
-      const int64_t nt = tile + gridDim.x;
-      if (nt < ntiles) {
-        const int64_t f0 = nt * EPB;
-        const int64_t nn = min64(EPB, p.n_el - f0);
-        prefetch_l2(p.q + f0 * n3, nn * n3 * sizeof(double));
-        prefetch_l2(p.fac + f0 * p.fac_estride, nn * p.fac_estride * sizeof(double));
-      }
-    }
+    if (tid == 0) prefetch_l2(p.fac + e0 * p.fac_estride, ne * p.fac_estride * sizeof(double));
     const bool act = el < ne;
     const int64_t e = e0 + el;
     double* const Ae = A + el * EA;
@@ -120,6 +116,13 @@ __global__ void __launch_bounds__(Cfg<kBP35, N>::NT)
     }
     __syncthreads();
     // ---- S3: metric chain rule on k-lines
+    if (tid == 0) {
+      const int64_t nt = tile + gridDim.x;
+      if (nt < ntiles) {
+        const int64_t f0 = nt * EPB;
+        prefetch_l2(p.q + f0 * n3, min64(EPB, p.n_el - f0) * n3 * sizeof(double));
+      }
+    }
     if (act) {
       const int j = ln / n, i = ln % n;
       double* b = Be + j * LB.s1 + i;

@@ -191,7 +191,7 @@ def make_operator(bp, degree, mesh, lam=0.0, variant="fused", device=None, facto
     stream = _stream(dev)
     with torch.cuda.device(dev):
         if factors is None:
-            verts = torch.from_numpy(np.ascontiguousarray(mesh.vertices)).to(dev)
+            verts = torch.from_numpy(np.array(mesh.vertices, dtype=np.float64)).to(dev)
             flag = torch.zeros(1, dtype=torch.int32, device=dev)
             _native.check(_native.lib().hx_geometric_factors(
                 plan.handle, _native.ptr(verts), n_el, 0, _native.ptr(packed),
@@ -215,7 +215,7 @@ def make_operator(bp, degree, mesh, lam=0.0, variant="fused", device=None, facto
             full = torch.empty(max(n_el, 1) * 7 * plan.slot_stride, dtype=torch.float64,
                                device=dev)
             s = _stream(dev)
-            v = torch.from_numpy(np.ascontiguousarray(mesh.vertices)).to(dev)
+            v = torch.from_numpy(np.array(mesh.vertices, dtype=np.float64)).to(dev)
             _native.check(_native.lib().hx_geometric_factors(
                 plan.handle, _native.ptr(v), n_el, 1, _native.ptr(full), None, s))
             out = torch.empty(n_el * 7 * q ** 3, dtype=torch.float64, device=dev)
@@ -277,7 +277,7 @@ def apply_operator(op, q, counters=None, threads=1, out=None):
     return result
 
 
-DEFAULT_CHUNK_BYTES = 32 << 20
+DEFAULT_CHUNK_BYTES = 8 << 20
 
 
 def host_chunk_elements(op, chunk_bytes=DEFAULT_CHUNK_BYTES):
