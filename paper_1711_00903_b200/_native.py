@@ -11,7 +11,8 @@ import os
 from .mesh import DegenerateGeometryError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libhexbench_b200.so")
+# HX_LIB_PATH selects an alternative build (tuning experiments only)
+LIB_PATH = os.environ.get("HX_LIB_PATH", os.path.join(HERE, "libhexbench_b200.so"))
 
 HX_OK, HX_EINVAL, HX_ENONFINITE, HX_EDEGENERATE, HX_ECUDA, HX_ENOMEM = range(6)
 HX_BP1, HX_BP35, HX_BP3 = 10, 35, 30

@@ -17,6 +17,14 @@
 #include "hx_common.cuh"
 #include "hx_plan.h"
 
+// HX_MINB_BP1 overrides Cfg<>::MINB (resident CTAs per SM for the register
+// budget) in tuning builds only.
+#ifdef HX_MINB_BP1
+#define HX_MINB_BP1_OF(N) HX_MINB_BP1
+#else
+#define HX_MINB_BP1_OF(N) Cfg<kBP1, N>::MINB
+#endif
+
 namespace hx {
 
 template <int N>
@@ -32,7 +40,7 @@ struct BP1Params {
 };
 
 template <int N>
-__global__ void __launch_bounds__(Cfg<kBP1, N>::NT)
+__global__ void __launch_bounds__(Cfg<kBP1, N>::NT, HX_MINB_BP1_OF(N))
     bp1_kernel(const __grid_constant__ BP1Params<N> p) {
   using C = Cfg<kBP1, N>;
   constexpr int n = N + 1, m = N + 2, n2 = n * n, n3 = n2 * n, m2 = m * m;

@@ -24,6 +24,17 @@
 #include "hx_common.cuh"
 #include "hx_plan.h"
 
+#ifndef HX_PF_BP3
+#define HX_PF_BP3 2  // stage at which a tile's factors are prefetched into L2
+#endif
+// HX_MINB_BP3 overrides Cfg<>::MINB (resident CTAs per SM for the register
+// budget) in tuning builds only.
+#ifdef HX_MINB_BP3
+#define HX_MINB_BP3_OF(N) HX_MINB_BP3
+#else
+#define HX_MINB_BP3_OF(N) Cfg<kBP3, N>::MINB
+#endif
+
 namespace hx {
 
 template <int N>
@@ -43,7 +54,7 @@ struct BP3Params {
 };
 
 template <int N>
-__global__ void __launch_bounds__(Cfg<kBP3, N>::NT)
+__global__ void __launch_bounds__(Cfg<kBP3, N>::NT, HX_MINB_BP3_OF(N))
     bp3_kernel(const __grid_constant__ BP3Params<N> p) {
   using C = Cfg<kBP3, N>;
   constexpr int n = N + 1, m = N + 2, n2 = n * n, n3 = n2 * n, m2 = m * m;
@@ -84,6 +95,8 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT)
     double* const Cc = Cs + el_c * EC;
 
     // ---- S1: j-lines (k, i): interpolate along s
+    if (HX_PF_BP3 == 1 && tid == 0) prefetch_l2(p.fac + e0 * fs, ne * fs * sizeof(double));
+    if (HX_PF_BP3 == 5 && tid == 0 && ne > 0) prefetch_l2(p.fac + e0 * fs, fs * sizeof(double));
     if (el_a < ne) {
       const int k = ln_a / n, i = ln_a % n;
       const double* src = p.q + (e0 + el_a) * n3 + k * n2 + i;
@@ -102,7 +115,8 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT)
     }
     __syncthreads();
     // ---- S2: i-lines (k, a): interpolate along r
-    if (tid == 0) prefetch_l2(p.fac + e0 * fs, ne * fs * sizeof(double));
+    if (HX_PF_BP3 == 2 && tid == 0) prefetch_l2(p.fac + e0 * fs, ne * fs * sizeof(double));
+    if (HX_PF_BP3 == 5 && tid == 0 && ne > 1) prefetch_l2(p.fac + (e0 + 1) * fs, fs * sizeof(double));
     if (el_b < ne) {
       const int k = ln_b / m, a = ln_b % m;
       const double* src = Ab + k * LX.s0 + a * LX.s1;
@@ -116,6 +130,9 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT)
     }
     __syncthreads();
     // ---- S3: k-lines (a, c): interpolate along t, differentiate along t
+    if (HX_PF_BP3 == 3 && tid == 0) prefetch_l2(p.fac + e0 * fs, ne * fs * sizeof(double));
+    if (HX_PF_BP3 == 5 && tid == 0 && ne > 2)
+      prefetch_l2(p.fac + (e0 + 2) * fs, (ne - 2) * fs * sizeof(double));
     double tv[m], tt[m], acc[m];
     const bool act_c = el_c < ne;
     const int ca = ln_c / m, cc = ln_c % m;
@@ -132,6 +149,7 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT)
     }
     __syncthreads();
     // ---- S4: r- and s-derivatives of T
+    if (HX_PF_BP3 == 4 && tid == 0) prefetch_l2(p.fac + e0 * fs, ne * fs * sizeof(double));
     if (act_c) {
       const int kk = ln_c / m, r = ln_c % m;
       double x[m], y[m];

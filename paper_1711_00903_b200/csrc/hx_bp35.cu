@@ -21,6 +21,17 @@
 #include "hx_common.cuh"
 #include "hx_plan.h"
 
+#ifndef HX_PF_BP35
+#define HX_PF_BP35 1  // stage at which a tile's factors are prefetched into L2
+#endif
+// HX_MINB_BP35 overrides Cfg<>::MINB (resident CTAs per SM for the register
+// budget) in tuning builds only.
+#ifdef HX_MINB_BP35
+#define HX_MINB_BP35_OF(N) HX_MINB_BP35
+#else
+#define HX_MINB_BP35_OF(N) Cfg<kBP35, N>::MINB
+#endif
+
 namespace hx {
 
 template <int N>
@@ -38,7 +49,7 @@ struct BP35Params {
 };
 
 template <int N>
-__global__ void __launch_bounds__(Cfg<kBP35, N>::NT)
+__global__ void __launch_bounds__(Cfg<kBP35, N>::NT, HX_MINB_BP35_OF(N))
     bp35_kernel(const __grid_constant__ BP35Params<N> p) {
   using C = Cfg<kBP35, N>;
   constexpr int n = N + 1, n2 = n * n, n3 = n2 * n;
@@ -70,7 +81,8 @@ __global__ void __launch_bounds__(Cfg<kBP35, N>::NT)
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t e0 = tile * EPB;
     const int ne = int(min64(EPB, p.n_el - e0));
-    if (tid == 0) prefetch_l2(p.fac + e0 * p.fac_estride, ne * p.fac_estride * sizeof(double));
+    if (HX_PF_BP35 == 1 && tid == 0)
+      prefetch_l2(p.fac + e0 * p.fac_estride, ne * p.fac_estride * sizeof(double));
     const bool act = el < ne;
     const int64_t e = e0 + el;
     double* const Ae = A + el * EA;
@@ -96,6 +108,8 @@ __global__ void __launch_bounds__(Cfg<kBP35, N>::NT)
     }
     __syncthreads();
     // ---- S2: r- and s-derivatives
+    if (HX_PF_BP35 == 2 && tid == 0)
+      prefetch_l2(p.fac + e0 * p.fac_estride, ne * p.fac_estride * sizeof(double));
     if (act) {
       const int k = ln / n, r = ln % n;
       double x[n], y[n];
