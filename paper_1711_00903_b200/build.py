@@ -57,7 +57,12 @@ def build(force=False, verbose=False, defines=(), lib=LIB):
     variant builds go to a separate path and never replace the product)."""
     if not force and not defines and lib == LIB and up_to_date():
         return LIB
-    build_dir = BUILD if not defines else os.path.join(BUILD, "v_" + "_".join(defines))
+    if defines:
+        import hashlib
+        tag = hashlib.sha1("|".join(defines).encode()).hexdigest()[:12]
+        build_dir = os.path.join(BUILD, "v_" + tag)
+    else:
+        build_dir = BUILD
     os.makedirs(build_dir, exist_ok=True)
     srcs = _sources()
     with ThreadPoolExecutor(max_workers=min(len(srcs), os.cpu_count() or 4)) as pool:

@@ -11,12 +11,11 @@
 //
 //   S1 j-lines (k,i)  n^2 : q (HBM)  -> I_s -> A as X[k][a][i]        L[0]
 //   S2 i-lines (k,a)  n*m : X -> I_r -> B as Y[k][a][c]                L[2]
-//   S3 k-lines (a,c)  m^2 : Y -> I_t -> t (regs), tt = D~_t t (regs),
-//                           t -> C as T[kk][a][c]                      L[4]
+//   S3 k-lines (a,c)  m^2 : Y -> I_t -> t -> C as T[kk][a][c]            L[4]
 //   S4 i-lines (kk,a) m^2 : T -> D~_r -> A as QR                       L[1]
 //      j-lines (kk,c) m^2 : T -> D~_s -> B as QS                       L[3]
-//   S5 k-lines (a,c)  m^2 : G (HBM) chain rule: rqr -> A, rqs -> B,
-//                           acc = lam GwJ t + D~_t^T rqt (regs)
+//   S5 k-lines (a,c)  m^2 : t from C, tt = D~_t t; G (HBM) chain rule:
+//                           rqr -> A, rqs -> B, acc = lam GwJ t + D~_t^T rqt
 //   S6 i-lines: A <- D~_r^T A        j-lines: B <- D~_s^T B
 //   S7 k-lines (a,c)  m^2 : acc += A + B;  I_t^T acc -> C as Z[k][a][c] L[5]
 //   S8 i-lines (k,a)  n*m : Z -> I_r^T -> A as W[k][a][i]              L[0]
@@ -24,6 +23,12 @@
 #include "hx_common.cuh"
 #include "hx_plan.h"
 
+// S5 re-reads T from shared memory instead of carrying t and D~_t t in
+// registers across two barriers: fewer live registers, +m^3 smem reads.
+// Pays at N >= 10 (tune02); below that the registers are available.
+#ifndef HX_BP3_REREAD_MIN_N
+#define HX_BP3_REREAD_MIN_N 10
+#endif
 #ifndef HX_PF_BP3
 #define HX_PF_BP3 2  // stage at which a tile's factors are prefetched into L2
 #endif
@@ -96,7 +101,6 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT, HX_MINB_BP3_OF(N))
 
     // ---- S1: j-lines (k, i): interpolate along s
     if (HX_PF_BP3 == 1 && tid == 0) prefetch_l2(p.fac + e0 * fs, ne * fs * sizeof(double));
-    if (HX_PF_BP3 == 5 && tid == 0 && ne > 0) prefetch_l2(p.fac + e0 * fs, fs * sizeof(double));
     if (el_a < ne) {
       const int k = ln_a / n, i = ln_a % n;
       const double* src = p.q + (e0 + el_a) * n3 + k * n2 + i;
@@ -116,7 +120,6 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT, HX_MINB_BP3_OF(N))
     __syncthreads();
     // ---- S2: i-lines (k, a): interpolate along r
     if (HX_PF_BP3 == 2 && tid == 0) prefetch_l2(p.fac + e0 * fs, ne * fs * sizeof(double));
-    if (HX_PF_BP3 == 5 && tid == 0 && ne > 1) prefetch_l2(p.fac + (e0 + 1) * fs, fs * sizeof(double));
     if (el_b < ne) {
       const int k = ln_b / m, a = ln_b % m;
       const double* src = Ab + k * LX.s0 + a * LX.s1;
@@ -129,20 +132,24 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT, HX_MINB_BP3_OF(N))
       for (int t = 0; t < m; ++t) dst[t] = y[t];
     }
     __syncthreads();
-    // ---- S3: k-lines (a, c): interpolate along t, differentiate along t
+    // ---- S3: k-lines (a, c): interpolate along t
     if (HX_PF_BP3 == 3 && tid == 0) prefetch_l2(p.fac + e0 * fs, ne * fs * sizeof(double));
-    if (HX_PF_BP3 == 5 && tid == 0 && ne > 2)
-      prefetch_l2(p.fac + (e0 + 2) * fs, (ne - 2) * fs * sizeof(double));
-    double tv[m], tt[m], acc[m];
+    double acc[m];
+    constexpr bool kReread = N >= HX_BP3_REREAD_MIN_N;
+    double tvc[kReread ? 1 : m], ttc[kReread ? 1 : m];  // carried S3 -> S5 unless kReread
     const bool act_c = el_c < ne;
     const int ca = ln_c / m, cc = ln_c % m;
     if (act_c) {
       const double* src = Bc + ca * LY.s1 + cc;
-      double x[n];
+      double x[n], tv[m];
 #pragma unroll
       for (int t = 0; t < n; ++t) x[t] = src[t * LY.s0];
       fold_apply<m, n, 1>(p.I, x, tv);
-      fold_apply<m, m, -1>(p.D, tv, tt);
+      if constexpr (!kReread) {
+#pragma unroll
+        for (int t = 0; t < m; ++t) tvc[t] = tv[t];
+        fold_apply<m, m, -1>(p.D, tvc, ttc);
+      }
       double* dst = Cc + ca * LT.s1 + cc;
 #pragma unroll
       for (int t = 0; t < m; ++t) dst[t * LT.s0] = tv[t];
@@ -174,7 +181,20 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT, HX_MINB_BP3_OF(N))
       double* qrl = Ac + ca * LQR.s1 + cc;
       double* qsl = Bc + ca * LQS.s1 + cc;
       const double* g = p.fac + (e0 + el_c) * fs + ln_c;
-      double rqt[m];
+      double rqt[m], tv[m], tt[m];
+      if constexpr (kReread) {
+        // re-read this thread's own T k-line (still intact in C)
+        const double* tl = Cc + ca * LT.s1 + cc;
+#pragma unroll
+        for (int t = 0; t < m; ++t) tv[t] = tl[t * LT.s0];
+        fold_apply<m, m, -1>(p.D, tv, tt);
+      } else {
+#pragma unroll
+        for (int t = 0; t < m; ++t) {
+          tv[t] = tvc[t];
+          tt[t] = ttc[t];
+        }
+      }
 #pragma unroll
       for (int t = 0; t < m; ++t) {
         const double* gk = g + t * m2;

@@ -16,7 +16,12 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+// tuning builds substitute an alternative generated table
+#ifdef HX_LAYOUTS_FILE
+#include HX_LAYOUTS_FILE
+#else
 #include "hx_layouts.h"
+#endif
 
 namespace hx {
 
@@ -112,6 +117,24 @@ __host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return
 __device__ __forceinline__ bool nonfinite(double v) {
   // exponent all ones <=> inf or nan
   return (__double_as_longlong(v) & 0x7ff0000000000000ll) == 0x7ff0000000000000ll;
+}
+
+// Load the j-line (k, i) = divmod(line, n) of one element's (n, n, n) field:
+// q[k][0..n-1][i] -- 8n-byte runs across the lanes of a warp.
+template <int n>
+__device__ __forceinline__ void load_jline(const double* qe, int line, double (&x)[n]) {
+  const double* src = qe + (line / n) * n * n + line % n;
+#pragma unroll
+  for (int t = 0; t < n; ++t) x[t] = src[t * n];
+}
+
+// Load the k-line (j, i) = divmod(line, n): q[0..n-1][j][i], coalesced over
+// consecutive lines.
+template <int n>
+__device__ __forceinline__ void load_kline(const double* qe, int line, double (&x)[n]) {
+  const double* src = qe + line;
+#pragma unroll
+  for (int t = 0; t < n; ++t) x[t] = src[t * n * n];
 }
 
 // Streaming store: the output is never re-read by the kernel, keep the

@@ -129,11 +129,23 @@ def perturb_mesh(mesh, amplitude=0.15, seed=0):
     verts = mesh.vertices + rng.uniform(-1, 1, mesh.vertices.shape) * amplitude * h / 2
     probe = np.array(list(itertools.product((-0.9, 0.0, 0.9), repeat=3)))
     g = _shape_gradients(probe[:, 0], probe[:, 1], probe[:, 2])  # (27, 8, 3)
-    for lo in range(0, mesh.n_el, 4096):
-        a = np.einsum("ecx,pcb->epxb", verts[lo:lo + 4096], g)
-        if np.any(np.abs(np.linalg.det(a)) <= DEGENERATE_DET):
+    for lo in range(0, mesh.n_el, 65536):
+        if np.any(np.abs(_det3(_jacobians(verts[lo:lo + 65536], g))) <= DEGENERATE_DET):
             raise DegenerateGeometryError("trilinear map is degenerate")
     return HexMesh(mesh.n_el, verts, mesh.extent)
+
+
+def _jacobians(verts, g):
+    """A[e, p, x, b] = sum_c verts[e, c, x] g[p, c, b] as one BLAS product."""
+    e, p = verts.shape[0], g.shape[0]
+    a = np.matmul(verts.transpose(0, 2, 1), g.transpose(1, 0, 2).reshape(8, p * 3))
+    return a.reshape(e, 3, p, 3).transpose(0, 2, 1, 3)
+
+
+def _det3(a):
+    return (a[..., 0, 0] * (a[..., 1, 1] * a[..., 2, 2] - a[..., 1, 2] * a[..., 2, 1])
+            - a[..., 0, 1] * (a[..., 1, 0] * a[..., 2, 2] - a[..., 1, 2] * a[..., 2, 0])
+            + a[..., 0, 2] * (a[..., 1, 0] * a[..., 2, 1] - a[..., 1, 1] * a[..., 2, 0]))
 
 
 def tensor_points(rule):
@@ -154,7 +166,7 @@ def geometric_factors(mesh, rule, chunk=2048):
     w3 = (w[:, None, None] * w[None, :, None] * w[None, None, :]).ravel()
     data = np.empty((mesh.n_el, 7, m ** 3))
     for lo in range(0, mesh.n_el, chunk):
-        a = np.einsum("ecx,pcb->epxb", mesh.vertices[lo:lo + chunk], g)
+        a = _jacobians(mesh.vertices[lo:lo + chunk], g)
         det = np.linalg.det(a)
         if np.any(det <= DEGENERATE_DET):
             raise DegenerateGeometryError("non-positive Jacobian determinant")

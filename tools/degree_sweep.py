@@ -1,0 +1,85 @@
+#!/usr/bin/env python3
+"""BASELINE config 4: N = 1..15 for BP1.0 / BP3.5 / BP3.0 at ~50 M DOF on one
+B200 (roofline fraction vs N).  Element counts per N follow SURVEY.md §8d
+(side^3 with side = 184, 123, 92, 74, 61, 53, 46, 41, 37, 33, 31, 28, 26, 25,
+23).  One JSON line per (bp, N); `--out` also writes them to a file.
+
+    python tools/degree_sweep.py [--degrees 1..15] [--steps 10] [--out file]
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+SIDES = {1: 184, 2: 123, 3: 92, 4: 74, 5: 61, 6: 53, 7: 46, 8: 41, 9: 37, 10: 33,
+         11: 31, 12: 28, 13: 26, 14: 25, 15: 23}
+
+
+def main():
+    import torch
+    import paper_1711_00903_b200 as hx
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--degrees", default="1..15")
+    ap.add_argument("--bps", default="BP1.0,BP3.5,BP3.0")
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--out", default=None)
+    args = ap.parse_args()
+    lo, hi = (int(x) for x in args.degrees.split("..")) if ".." in args.degrees \
+        else (int(args.degrees),) * 2
+    peak = 6554.9
+    pk = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                      "MEASURED_PEAKS.json")
+    if os.path.exists(pk):
+        peak = json.load(open(pk))["hbm_gbs"]
+    fh = open(args.out, "a") if args.out else None
+    for deg in range(lo, hi + 1):
+        cache = f"/tmp/hx_mesh_{SIDES[deg]}.npy"
+        if os.path.exists(cache):
+            v = np.load(cache)
+            mesh = hx.HexMesh(v.shape[0], v, 2.0)
+        else:
+            mesh = hx.perturb_mesh(hx.build_cube_mesh(SIDES[deg], 2.0), amplitude=0.15, seed=7)
+            np.save(cache, mesh.vertices)
+        for bp in args.bps.split(","):
+            op = hx.make_operator(bp, deg, mesh, lam=1.0)
+            q = torch.randn(mesh.n_el, op.n_p, dtype=torch.float64, device="cuda")
+            out = torch.empty_like(q)
+            for _ in range(args.warmup):
+                hx.apply_device(op, q, out)
+            torch.cuda.synchronize()
+            ev = []
+            for _ in range(args.steps):
+                s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                s.record()
+                hx.apply_device(op, q, out)
+                e.record()
+                ev.append((s, e))
+            torch.cuda.synchronize()
+            ms = statistics.median(s.elapsed_time(e) for s, e in ev)
+            t = hx.traffic(bp, deg, mesh.n_el)
+            nbytes = t.bytes_per_element * mesh.n_el
+            rec = {"bp": bp, "degree": deg, "n_el": mesh.n_el, "dofs": mesh.n_el * op.n_p,
+                   "ms": ms, "gdof_per_s": mesh.n_el * op.n_p / ms / 1e6,
+                   "gb_per_s": nbytes / ms / 1e6, "frac_of_measured_peak": nbytes / ms / 1e6 / peak,
+                   "gflop_per_s": hx.flop_model(bp, "fused", deg) * mesh.n_el / ms / 1e6,
+                   "threads": op.plan.threads, "elements_per_tile": op.plan.elements_per_tile,
+                   "smem_bytes": op.plan.smem_bytes,
+                   "lib": os.path.basename(os.environ.get("HX_LIB_PATH", "default"))}
+            line = json.dumps(rec)
+            print(line, flush=True)
+            if fh:
+                fh.write(line + "\n")
+                fh.flush()
+            del op, q, out
+            torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    main()

@@ -32,4 +32,10 @@ if [[ $STAGES == *ncu* ]]; then
       python tools/profile_one.py "$K" > "$OUT/ncu_${K}.log" 2>&1
   done
 fi
+if [[ $STAGES == *sweep* ]]; then
+  timeout 1500 python tools/degree_sweep.py --out "$OUT/degree_sweep.jsonl" > "$OUT/degree_sweep.log" 2>&1
+fi
+if [[ $STAGES == *probe* ]]; then
+  timeout 120 ./tools/fp64_probe > "$OUT/fp64_probe.txt" 2>&1
+fi
 echo done > "$OUT/DONE"
