@@ -95,6 +95,31 @@ int hx_apply_host(const hx_plan* plan, const double* q_host, const double* facto
                   double* out_host, int64_t n_el, int64_t chunk_el, void* work,
                   int* status_flag, void* stream);
 
+/* apply + <q, A q>: as hx_apply, and *energy (device double) receives
+ * <q, A q>, evaluated inside the kernel from its quadrature-point values
+ * (grad q . G grad q + lam GwJ q^2; GwJ (I q)^2 for BP1.0) -- no extra pass
+ * over q or out.  `partials` is device scratch of n_partials >=
+ * hx_energy_partials() doubles.  New: the reference has no solver; this
+ * serves the CG driver.                       */
+int64_t hx_energy_partials(void);
+int hx_apply_energy(const hx_plan* plan, const double* q, const double* factors, double* out,
+                    int64_t n_el, double* partials, int64_t n_partials, double* energy,
+                    int* status_flag, void* stream);
+
+/* CG vector kernels on device arrays of n doubles; scalars are device
+ * pointers so an iteration never synchronises with the host.
+ *   hx_dot:          *result = <u, v>
+ *   hx_cg_update:    alpha = *rr / *pap; x += alpha p; r -= alpha ap; *rr_new = <r, r>
+ *   hx_cg_direction: p = r + (*rr_new / *rr_old) p
+ * Reductions are fixed-order (bitwise reproducible).                        */
+int hx_dot(const double* u, const double* v, int64_t n, double* partials, int64_t n_partials,
+           double* result, void* stream);
+int hx_cg_update(double* x, const double* p, double* r, const double* ap, int64_t n,
+                 const double* rr, const double* pap, double* partials, int64_t n_partials,
+                 double* rr_new, void* stream);
+int hx_cg_direction(double* p, const double* r, int64_t n, const double* rr_new,
+                    const double* rr_old, void* stream);
+
 /* Elements each CTA processes per tile, threads per CTA and dynamic shared
  * memory bytes of the plan's kernel (for reports and tests).                */
 int hx_plan_kernel_shape(const hx_plan* plan, int* elements_per_tile, int* threads,

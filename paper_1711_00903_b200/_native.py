@@ -36,6 +36,11 @@ SIGNATURES = {
     "hx_plan_kernel_shape": (_c.c_int, [_P, _c.POINTER(_c.c_int), _c.POINTER(_c.c_int),
                                         _c.POINTER(_c.c_int)]),
     "hx_measure_smem_bandwidth": (_c.c_int, [_c.POINTER(_c.c_double), _P]),
+    "hx_energy_partials": (_c.c_int64, []),
+    "hx_apply_energy": (_c.c_int, [_P, _P, _P, _P, _c.c_int64, _P, _c.c_int64, _P, _P, _P]),
+    "hx_dot": (_c.c_int, [_P, _P, _c.c_int64, _P, _c.c_int64, _P, _P]),
+    "hx_cg_update": (_c.c_int, [_P, _P, _P, _P, _c.c_int64, _P, _P, _P, _c.c_int64, _P, _P]),
+    "hx_cg_direction": (_c.c_int, [_P, _P, _c.c_int64, _P, _P, _P]),
     "hx_strerror": (_c.c_char_p, [_c.c_int]),
     "hx_device_ok": (_c.c_int, []),
 }

@@ -37,9 +37,10 @@ struct BP1Params {
   int64_t n_el;
   int64_t fac_estride;
   int* flag;
+  double* energy;  // per-CTA partials of <q, A q> (ENERGY instantiation only)
 };
 
-template <int N>
+template <int N, bool ENERGY>
 __global__ void __launch_bounds__(Cfg<kBP1, N>::NT, HX_MINB_BP1_OF(N))
     bp1_kernel(const __grid_constant__ BP1Params<N> p) {
   using C = Cfg<kBP1, N>;
@@ -67,6 +68,7 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT, HX_MINB_BP1_OF(N))
   const int el_b = tid / (n * m), ln_b = tid % (n * m);  // n*m lines (S2, S4)
   const int el_c = tid / m2, ln_c = tid % m2;  // m^2 lines (S3)
 
+  double en = 0.0;  // this thread's share of <q, A q> (ENERGY)
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t e0 = tile * EPB;
     const int ne = int(min64(EPB, p.n_el - e0));
@@ -127,7 +129,11 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT, HX_MINB_BP1_OF(N))
       for (int t = 0; t < n; ++t) x[t] = line[t * LY.s0];
       fold_apply<m, n, 1>(p.I, x, y);
 #pragma unroll
-      for (int t = 0; t < m; ++t) y[t] *= w[t];
+      for (int t = 0; t < m; ++t) {
+        const double wy = y[t] * w[t];
+        if constexpr (ENERGY) en += wy * y[t];  // <q, A q> = sum GwJ (I q)^2
+        y[t] = wy;
+      }
       fold_apply<n, m, 1>(p.It, y, x);
 #pragma unroll
       for (int t = 0; t < n; ++t) line[t * LY.s0] = x[t];
@@ -160,24 +166,38 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT, HX_MINB_BP1_OF(N))
     }
     __syncthreads();  // X is rewritten by the next tile's S1
   }
+  if constexpr (ENERGY) {
+    const double sum = block_sum<C::NT>(en, X);
+    if (tid == 0) p.energy[blockIdx.x] = sum;
+  }
 }
 
-template <int N>
-static cudaError_t launch_n(const hx_plan& P, const double* q, const double* fac, double* out,
-                            int64_t n_el, int* flag, cudaStream_t s) {
+template <int N, bool E, class Prm>
+static cudaError_t launch_t(const Prm& prm, int64_t n_el, cudaStream_t s) {
   using C = Cfg<kBP1, N>;
-  constexpr int n = N + 1, m = N + 2;
   constexpr int smem = smem_doubles<kBP1, N>() * int(sizeof(double));
   static int blocks_per_sm = -1;
   if (blocks_per_sm < 0) {
-    cudaError_t err = cudaFuncSetAttribute(bp1_kernel<N>,
+    cudaError_t err = cudaFuncSetAttribute(bp1_kernel<N, E>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (err != cudaSuccess) return err;
-    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, bp1_kernel<N>, C::NT,
+    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, bp1_kernel<N, E>, C::NT,
                                                         smem);
     if (err != cudaSuccess) return err;
     if (blocks_per_sm < 1) blocks_per_sm = 1;
   }
+  const int64_t ntiles = (n_el + C::EPB - 1) / C::EPB;
+  const int64_t grid = min64(ntiles, int64_t(blocks_per_sm) * sm_count());
+  bp1_kernel<N, E><<<unsigned(grid), C::NT, smem, s>>>(prm);
+  return cudaGetLastError();
+}
+
+template <int N>
+static cudaError_t launch_n(const hx_plan& P, const double* q, const double* fac, double* out,
+                            int64_t n_el, int* flag, double* energy, cudaStream_t s) {
+  using C = Cfg<kBP1, N>;
+  constexpr int n = N + 1, m = N + 2;
+  constexpr int smem = smem_doubles<kBP1, N>() * int(sizeof(double));
   BP1Params<N> prm;
   double it[n * m];
   fill_fold(prm.I, P.interp);
@@ -189,18 +209,16 @@ static cudaError_t launch_n(const hx_plan& P, const double* q, const double* fac
   prm.n_el = n_el;
   prm.fac_estride = P.elem_stride;
   prm.flag = flag;
-  const int64_t ntiles = (n_el + C::EPB - 1) / C::EPB;
-  const int64_t grid = min64(ntiles, int64_t(blocks_per_sm) * sm_count());
-  bp1_kernel<N><<<unsigned(grid), C::NT, smem, s>>>(prm);
-  return cudaGetLastError();
+  prm.energy = energy;
+  return energy ? launch_t<N, true>(prm, n_el, s) : launch_t<N, false>(prm, n_el, s);
 }
 
 cudaError_t launch_bp1(const hx_plan& P, const double* q, const double* fac, double* out,
-                       int64_t n_el, int* flag, cudaStream_t s) {
+                       int64_t n_el, int* flag, double* energy, cudaStream_t s) {
   switch (P.degree) {
 #define HX_CASE(N) \
   case N:          \
-    return launch_n<N>(P, q, fac, out, n_el, flag, s);
+    return launch_n<N>(P, q, fac, out, n_el, flag, energy, s);
     HX_CASE(1) HX_CASE(2) HX_CASE(3) HX_CASE(4) HX_CASE(5) HX_CASE(6) HX_CASE(7) HX_CASE(8)
     HX_CASE(9) HX_CASE(10) HX_CASE(11) HX_CASE(12) HX_CASE(13) HX_CASE(14) HX_CASE(15)
 #undef HX_CASE

@@ -25,9 +25,9 @@
 
 // S5 re-reads T from shared memory instead of carrying t and D~_t t in
 // registers across two barriers: fewer live registers, +m^3 smem reads.
-// Pays at N >= 10 (tune02); below that the registers are available.
+// Pays at N >= 7 (tune02, tune05); below that the registers are available.
 #ifndef HX_BP3_REREAD_MIN_N
-#define HX_BP3_REREAD_MIN_N 10
+#define HX_BP3_REREAD_MIN_N 7
 #endif
 #ifndef HX_PF_BP3
 #define HX_PF_BP3 2  // stage at which a tile's factors are prefetched into L2
@@ -56,9 +56,10 @@ struct BP3Params {
   int64_t fac_sstride;
   double lam;
   int* flag;
+  double* energy;  // per-CTA partials of <q, A q> (ENERGY instantiation only)
 };
 
-template <int N>
+template <int N, bool ENERGY>
 __global__ void __launch_bounds__(Cfg<kBP3, N>::NT, HX_MINB_BP3_OF(N))
     bp3_kernel(const __grid_constant__ BP3Params<N> p) {
   using C = Cfg<kBP3, N>;
@@ -88,6 +89,7 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT, HX_MINB_BP3_OF(N))
   const int el_b = tid / (n * m), ln_b = tid % (n * m);
   const int el_c = tid / m2, ln_c = tid % m2;
 
+  double en = 0.0;  // this thread's share of <q, A q> (ENERGY)
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t e0 = tile * EPB;
     const int ne = int(min64(EPB, p.n_el - e0));
@@ -202,10 +204,15 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT, HX_MINB_BP3_OF(N))
         const double gss = gk[3 * ss], gst = gk[4 * ss], gtt = gk[5 * ss];
         const double gwj = gk[6 * ss];
         const double qr = qrl[t * LQR.s0], qs = qsl[t * LQS.s0], qt = tt[t];
-        qrl[t * LQR.s0] = grr * qr + grs * qs + grt * qt;
-        qsl[t * LQS.s0] = grs * qr + gss * qs + gst * qt;
+        const double rqr = grr * qr + grs * qs + grt * qt;
+        const double rqs = grs * qr + gss * qs + gst * qt;
+        qrl[t * LQR.s0] = rqr;
+        qsl[t * LQS.s0] = rqs;
         rqt[t] = grt * qr + gst * qs + gtt * qt;
-        tv[t] = p.lam * gwj * tv[t];
+        const double lt = p.lam * gwj * tv[t];
+        // <q, A q> = sum over GL points of grad t . G grad t + lam GwJ t^2
+        if constexpr (ENERGY) en += qr * rqr + qs * rqs + qt * rqt[t] + tv[t] * lt;
+        tv[t] = lt;
       }
       fold_apply<m, m, -1>(p.Dt, rqt, acc);
 #pragma unroll
@@ -277,24 +284,38 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT, HX_MINB_BP3_OF(N))
     }
     __syncthreads();  // A is rewritten by the next tile's S1
   }
+  if constexpr (ENERGY) {
+    const double sum = block_sum<C::NT>(en, A);
+    if (tid == 0) p.energy[blockIdx.x] = sum;
+  }
 }
 
-template <int N>
-static cudaError_t launch_n(const hx_plan& P, const double* q, const double* fac, double* out,
-                            int64_t n_el, int* flag, cudaStream_t s) {
+template <int N, bool E, class Prm>
+static cudaError_t launch_t(const Prm& prm, int64_t n_el, cudaStream_t s) {
   using C = Cfg<kBP3, N>;
-  constexpr int n = N + 1, m = N + 2;
   constexpr int smem = smem_doubles<kBP3, N>() * int(sizeof(double));
   static int blocks_per_sm = -1;
   if (blocks_per_sm < 0) {
-    cudaError_t err = cudaFuncSetAttribute(bp3_kernel<N>,
+    cudaError_t err = cudaFuncSetAttribute(bp3_kernel<N, E>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (err != cudaSuccess) return err;
-    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, bp3_kernel<N>, C::NT,
+    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, bp3_kernel<N, E>, C::NT,
                                                         smem);
     if (err != cudaSuccess) return err;
     if (blocks_per_sm < 1) blocks_per_sm = 1;
   }
+  const int64_t ntiles = (n_el + C::EPB - 1) / C::EPB;
+  const int64_t grid = min64(ntiles, int64_t(blocks_per_sm) * sm_count());
+  bp3_kernel<N, E><<<unsigned(grid), C::NT, smem, s>>>(prm);
+  return cudaGetLastError();
+}
+
+template <int N>
+static cudaError_t launch_n(const hx_plan& P, const double* q, const double* fac, double* out,
+                            int64_t n_el, int* flag, double* energy, cudaStream_t s) {
+  using C = Cfg<kBP3, N>;
+  constexpr int n = N + 1, m = N + 2;
+  constexpr int smem = smem_doubles<kBP3, N>() * int(sizeof(double));
   BP3Params<N> prm;
   double it[n * m], dt[m * m];
   fill_fold(prm.I, P.interp);
@@ -311,18 +332,16 @@ static cudaError_t launch_n(const hx_plan& P, const double* q, const double* fac
   prm.fac_sstride = P.slot_stride;
   prm.lam = P.lam;
   prm.flag = flag;
-  const int64_t ntiles = (n_el + C::EPB - 1) / C::EPB;
-  const int64_t grid = min64(ntiles, int64_t(blocks_per_sm) * sm_count());
-  bp3_kernel<N><<<unsigned(grid), C::NT, smem, s>>>(prm);
-  return cudaGetLastError();
+  prm.energy = energy;
+  return energy ? launch_t<N, true>(prm, n_el, s) : launch_t<N, false>(prm, n_el, s);
 }
 
 cudaError_t launch_bp3(const hx_plan& P, const double* q, const double* fac, double* out,
-                       int64_t n_el, int* flag, cudaStream_t s) {
+                       int64_t n_el, int* flag, double* energy, cudaStream_t s) {
   switch (P.degree) {
 #define HX_CASE(N) \
   case N:          \
-    return launch_n<N>(P, q, fac, out, n_el, flag, s);
+    return launch_n<N>(P, q, fac, out, n_el, flag, energy, s);
     HX_CASE(1) HX_CASE(2) HX_CASE(3) HX_CASE(4) HX_CASE(5) HX_CASE(6) HX_CASE(7) HX_CASE(8)
     HX_CASE(9) HX_CASE(10) HX_CASE(11) HX_CASE(12) HX_CASE(13) HX_CASE(14) HX_CASE(15)
 #undef HX_CASE

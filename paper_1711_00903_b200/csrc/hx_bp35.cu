@@ -46,9 +46,10 @@ struct BP35Params {
   int64_t fac_sstride;  // doubles per slot
   double lam;
   int* flag;
+  double* energy;  // per-CTA partials of <q, A q> (ENERGY instantiation only)
 };
 
-template <int N>
+template <int N, bool ENERGY>
 __global__ void __launch_bounds__(Cfg<kBP35, N>::NT, HX_MINB_BP35_OF(N))
     bp35_kernel(const __grid_constant__ BP35Params<N> p) {
   using C = Cfg<kBP35, N>;
@@ -78,6 +79,7 @@ __global__ void __launch_bounds__(Cfg<kBP35, N>::NT, HX_MINB_BP35_OF(N))
     prefetch_l2(p.q + e0 * n3, ne * n3 * sizeof(double));
   }
 
+  double en = 0.0;  // this thread's share of <q, A q> (ENERGY)
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t e0 = tile * EPB;
     const int ne = int(min64(EPB, p.n_el - e0));
@@ -150,10 +152,15 @@ __global__ void __launch_bounds__(Cfg<kBP35, N>::NT, HX_MINB_BP35_OF(N))
         const double gss = gk[3 * ss], gst = gk[4 * ss], gtt = gk[5 * ss];
         const double gwj = gk[6 * ss];
         const double qr = b[k * LB.s0], qs = c[k * LC.s0], qtk = qt[k];
-        b[k * LB.s0] = grr * qr + grs * qs + grt * qtk;
-        c[k * LC.s0] = grs * qr + gss * qs + gst * qtk;
+        const double rqr = grr * qr + grs * qs + grt * qtk;
+        const double rqs = grs * qr + gss * qs + gst * qtk;
+        b[k * LB.s0] = rqr;
+        c[k * LC.s0] = rqs;
         rqt[k] = grt * qr + gst * qs + gtt * qtk;
-        qv[k] = p.lam * gwj * qv[k];
+        const double lq = p.lam * gwj * qv[k];
+        // <q, A q> = sum over points of grad q . G grad q + lam GwJ q^2
+        if constexpr (ENERGY) en += qr * rqr + qs * rqs + qtk * rqt[k] + qv[k] * lq;
+        qv[k] = lq;
       }
       fold_apply<n, n, -1>(p.Dt, rqt, acc);
 #pragma unroll
@@ -190,23 +197,35 @@ __global__ void __launch_bounds__(Cfg<kBP35, N>::NT, HX_MINB_BP35_OF(N))
     // A is rewritten by the next tile's S1 only after it has passed this
     // tile's S3/S4 barriers; B and C only after the next S1 barrier.
   }
+  if constexpr (ENERGY) {
+    const double sum = block_sum<C::NT>(en, A);  // A is idle after the last S3
+    if (tid == 0) p.energy[blockIdx.x] = sum;
+  }
 }
 
-template <int N>
-static cudaError_t launch_n(const hx_plan& P, const double* q, const double* fac, double* out,
-                            int64_t n_el, int* flag, cudaStream_t s) {
+template <int N, bool E, class Prm>
+static cudaError_t launch_t(const Prm& prm, int64_t n_el, cudaStream_t s) {
   using C = Cfg<kBP35, N>;
   constexpr int smem = smem_doubles<kBP35, N>() * int(sizeof(double));
   static int blocks_per_sm = -1;
   if (blocks_per_sm < 0) {
-    cudaError_t err = cudaFuncSetAttribute(bp35_kernel<N>,
+    cudaError_t err = cudaFuncSetAttribute(bp35_kernel<N, E>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (err != cudaSuccess) return err;
-    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, bp35_kernel<N>, C::NT,
+    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, bp35_kernel<N, E>, C::NT,
                                                         smem);
     if (err != cudaSuccess) return err;
     if (blocks_per_sm < 1) blocks_per_sm = 1;
   }
+  const int64_t ntiles = (n_el + C::EPB - 1) / C::EPB;
+  const int64_t grid = min64(ntiles, int64_t(blocks_per_sm) * sm_count());
+  bp35_kernel<N, E><<<unsigned(grid), C::NT, smem, s>>>(prm);
+  return cudaGetLastError();
+}
+
+template <int N>
+static cudaError_t launch_n(const hx_plan& P, const double* q, const double* fac, double* out,
+                            int64_t n_el, int* flag, double* energy, cudaStream_t s) {
   BP35Params<N> prm;
   constexpr int n = N + 1;
   double dt[n * n];
@@ -221,18 +240,16 @@ static cudaError_t launch_n(const hx_plan& P, const double* q, const double* fac
   prm.fac_sstride = P.slot_stride;
   prm.lam = P.lam;
   prm.flag = flag;
-  const int64_t ntiles = (n_el + C::EPB - 1) / C::EPB;
-  const int64_t grid = min64(ntiles, int64_t(blocks_per_sm) * sm_count());
-  bp35_kernel<N><<<unsigned(grid), C::NT, smem, s>>>(prm);
-  return cudaGetLastError();
+  prm.energy = energy;
+  return energy ? launch_t<N, true>(prm, n_el, s) : launch_t<N, false>(prm, n_el, s);
 }
 
 cudaError_t launch_bp35(const hx_plan& P, const double* q, const double* fac, double* out,
-                        int64_t n_el, int* flag, cudaStream_t s) {
+                        int64_t n_el, int* flag, double* energy, cudaStream_t s) {
   switch (P.degree) {
 #define HX_CASE(N) \
   case N:          \
-    return launch_n<N>(P, q, fac, out, n_el, flag, s);
+    return launch_n<N>(P, q, fac, out, n_el, flag, energy, s);
     HX_CASE(1) HX_CASE(2) HX_CASE(3) HX_CASE(4) HX_CASE(5) HX_CASE(6) HX_CASE(7) HX_CASE(8)
     HX_CASE(9) HX_CASE(10) HX_CASE(11) HX_CASE(12) HX_CASE(13) HX_CASE(14) HX_CASE(15)
 #undef HX_CASE

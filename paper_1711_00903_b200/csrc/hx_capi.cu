@@ -42,15 +42,15 @@ static int kernel_shape(int bp, int degree, int* epb, int* nt, int* smem) {
 }
 
 static cudaError_t launch(const hx_plan& P, const double* q, const double* fac, double* out,
-                          int64_t n_el, int* flag, cudaStream_t s) {
+                          int64_t n_el, int* flag, cudaStream_t s, double* energy = nullptr) {
   if (n_el == 0) return cudaSuccess;
   switch (P.bp) {
     case HX_BP1:
-      return launch_bp1(P, q, fac, out, n_el, flag, s);
+      return launch_bp1(P, q, fac, out, n_el, flag, energy, s);
     case HX_BP35:
-      return launch_bp35(P, q, fac, out, n_el, flag, s);
+      return launch_bp35(P, q, fac, out, n_el, flag, energy, s);
     default:
-      return launch_bp3(P, q, fac, out, n_el, flag, s);
+      return launch_bp3(P, q, fac, out, n_el, flag, energy, s);
   }
 }
 
@@ -219,6 +219,45 @@ int hx_apply_host(const hx_plan* Pc, const double* q_host, const double* factors
   if (nchunks >= 2) cudaStreamWaitEvent(caller, e_out[nchunks & 1], 0);
   cudaEventDestroy(start);
   return cuda_status(cudaGetLastError());
+}
+
+int64_t hx_energy_partials(void) { return int64_t(32) * sm_count(); }
+
+int hx_apply_energy(const hx_plan* P, const double* q, const double* factors, double* out,
+                    int64_t n_el, double* partials, int64_t n_partials, double* energy,
+                    int* flag, void* stream) {
+  if (!P || n_el < 0 || !partials || !energy) return HX_EINVAL;
+  if (n_el > 0 && (!q || !factors || !out)) return HX_EINVAL;
+  if (n_partials < hx_energy_partials()) return HX_EINVAL;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t err = cudaMemsetAsync(partials, 0, sizeof(double) * n_partials, s);
+  if (err == cudaSuccess) err = launch(*P, q, factors, out, n_el, flag, s, partials);
+  if (err == cudaSuccess) err = launch_sum(partials, int(n_partials), energy, s);
+  return cuda_status(err);
+}
+
+int hx_dot(const double* u, const double* v, int64_t n, double* partials, int64_t n_partials,
+           double* result, void* stream) {
+  if (n < 0 || !partials || !result || (n > 0 && (!u || !v))) return HX_EINVAL;
+  if (n_partials < hx_energy_partials()) return HX_EINVAL;
+  return cuda_status(launch_dot(u, v, n, partials, result, static_cast<cudaStream_t>(stream)));
+}
+
+int hx_cg_update(double* x, const double* p, double* r, const double* ap, int64_t n,
+                 const double* rr, const double* pap, double* partials, int64_t n_partials,
+                 double* rr_new, void* stream) {
+  if (n < 0 || !rr || !pap || !partials || !rr_new) return HX_EINVAL;
+  if (n > 0 && (!x || !p || !r || !ap)) return HX_EINVAL;
+  if (n_partials < hx_energy_partials()) return HX_EINVAL;
+  return cuda_status(launch_cg_update(x, p, r, ap, n, rr, pap, partials, rr_new,
+                                      static_cast<cudaStream_t>(stream)));
+}
+
+int hx_cg_direction(double* p, const double* r, int64_t n, const double* rr_new,
+                    const double* rr_old, void* stream) {
+  if (n < 0 || !rr_new || !rr_old || (n > 0 && (!p || !r))) return HX_EINVAL;
+  return cuda_status(launch_cg_direction(p, r, n, rr_new, rr_old,
+                                         static_cast<cudaStream_t>(stream)));
 }
 
 int hx_measure_smem_bandwidth(double* bytes_per_s, void* stream) {

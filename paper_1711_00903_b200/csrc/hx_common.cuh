@@ -141,6 +141,22 @@ __device__ __forceinline__ void load_kline(const double* qe, int line, double (&
 // prefetched inputs resident in L2 instead.
 __device__ __forceinline__ void st_stream(double* p, double v) { __stcs(p, v); }
 
+// Sum of one double per thread over the CTA (result valid in thread 0).
+// `scratch` is shared memory of at least NT/32 doubles that no thread is
+// still reading.
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double* scratch) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) scratch[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < (NT + 31) / 32; ++w) s += scratch[w];
+  return s;
+}
+
 template <int BP, int N>
 constexpr int smem_doubles() {
   using C = Cfg<BP, N>;

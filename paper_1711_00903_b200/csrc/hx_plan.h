@@ -35,16 +35,24 @@ namespace hx {
 
 // launch the fused element kernel for elements [0, n_el) of device arrays
 cudaError_t launch_bp1(const hx_plan& P, const double* q, const double* fac, double* out,
-                       int64_t n_el, int* flag, cudaStream_t s);
+                       int64_t n_el, int* flag, double* energy, cudaStream_t s);
 cudaError_t launch_bp35(const hx_plan& P, const double* q, const double* fac, double* out,
-                        int64_t n_el, int* flag, cudaStream_t s);
+                        int64_t n_el, int* flag, double* energy, cudaStream_t s);
 cudaError_t launch_bp3(const hx_plan& P, const double* q, const double* fac, double* out,
-                       int64_t n_el, int* flag, cudaStream_t s);
+                       int64_t n_el, int* flag, double* energy, cudaStream_t s);
 cudaError_t launch_geometry(const hx_plan& P, const double* verts, int64_t n_el, int all_slots,
                             double* fac, int* flag, cudaStream_t s);
 cudaError_t launch_repack(const hx_plan& P, const double* src, int64_t n_el, double* dst,
                           int to_packed, cudaStream_t s);
 cudaError_t launch_smem_probe(double* sink, int iters, float* ms, cudaStream_t s);
+cudaError_t launch_sum(const double* part, int n, double* out, cudaStream_t s);
+cudaError_t launch_dot(const double* u, const double* v, int64_t n, double* part,
+                       double* result, cudaStream_t s);
+cudaError_t launch_cg_update(double* x, const double* p, double* r, const double* ap, int64_t n,
+                             const double* rr, const double* pap, double* part, double* rr_new,
+                             cudaStream_t s);
+cudaError_t launch_cg_direction(double* p, const double* r, int64_t n, const double* rr_new,
+                                const double* rr_old, cudaStream_t s);
 
 int sm_count();
 
