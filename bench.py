@@ -316,6 +316,75 @@ def e2e_report(op, mesh, steps, warmup):
                         f"H2D/kernel/D2H pipeline, chunk {chunk} elements"}
 
 
+def pcie_bandwidth(nbytes, trials=5):
+    """Pinned host<->device copy rates (GB/s) at the e2e step size: H2D alone,
+    D2H alone, and the time of both directions concurrently (the PCIe bound
+    of one e2e step)."""
+    import torch
+
+    n = nbytes // 8
+    h_in = torch.empty(n, dtype=torch.float64).pin_memory()
+    h_out = torch.empty(n, dtype=torch.float64).pin_memory()
+    d_in = torch.empty(n, dtype=torch.float64, device="cuda")
+    d_out = torch.zeros(n, dtype=torch.float64, device="cuda")
+    s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+
+    def timed(fn):
+        best = float("inf")
+        for _ in range(trials):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            fn()
+            torch.cuda.synchronize()
+            best = min(best, time.perf_counter() - t0)
+        return best
+
+    def both():
+        with torch.cuda.stream(s_in):
+            d_in.copy_(h_in, non_blocking=True)
+        with torch.cuda.stream(s_out):
+            h_out.copy_(d_out, non_blocking=True)
+
+    t_h2d = timed(lambda: d_in.copy_(h_in, non_blocking=True))
+    t_d2h = timed(lambda: h_out.copy_(d_out, non_blocking=True))
+    t_both = timed(both)
+    return {"h2d_gb_per_s": nbytes / t_h2d / 1e9, "d2h_gb_per_s": nbytes / t_d2h / 1e9,
+            "bidirectional_ms": t_both * 1e3}
+
+
+def cg_report(op, mesh, iters=20, warmup=3):
+    """CG iteration throughput (paper_1711_00903_b200/cg.py): fused matvec +
+    <p,Ap>, update, direction -- 3 kernels per iteration plus 2 tiny reduces,
+    no host synchronisation.  HBM traffic per iteration = the matvec's Table-1
+    bytes + 9 vector passes (x, p, r, Ap reads/writes)."""
+    import torch
+    import paper_1711_00903_b200 as hx
+    from paper_1711_00903_b200.cg import CGWorkspace, cg_iterations
+
+    b = torch.randn(op.n_el, op.n_p, dtype=torch.float64, device="cuda")
+    w = CGWorkspace(b)
+    cg_iterations(op, b, warmup, w)
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    cg_iterations(op, b, iters, w)
+    e.record()
+    e.synchronize()
+    # subtract the per-call setup (two copies + one dot) measured separately
+    s0, e0 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record()
+    cg_iterations(op, b, 0, w)
+    e0.record()
+    e0.synchronize()
+    ms = (s.elapsed_time(e) - s0.elapsed_time(e0)) / iters
+    per_el = hx.traffic(op.bp, op.degree).bytes_per_element + 9 * 8 * op.n_p
+    gbs = per_el * op.n_el / (ms * 1e-3) / 1e9
+    return {"bp": op.bp, "degree": op.degree, "n_el": op.n_el, "ms_per_iteration": ms,
+            "gdof_iterations_per_s": op.n_el * op.n_p / (ms * 1e-3) / 1e9,
+            "hbm_bytes_per_iteration": per_el * op.n_el, "achieved_gb_per_s": gbs,
+            "kernels_per_iteration": 5}
+
+
 def run_ours(args):
     import torch
     import paper_1711_00903_b200 as hx
@@ -360,6 +429,23 @@ def run_ours(args):
     e2e_ms = max_over_ranks(e2e_ms, world)
     e2e["value"] = dofs_all / (e2e_ms * 1e-3) / 1e9
     e2e["ms_per_step"] = e2e_ms
+    if rank == 0 and not args.quick:
+        pcie = pcie_bandwidth(e2e["h2d_bytes_per_step"])
+        e2e["pcie"] = pcie
+        e2e["frac_of_pcie_bound"] = pcie["bidirectional_ms"] / e2e_ms
+    cg = cg_report(op, mesh) if (rank == 0 and not args.quick) else None
+    calib = None
+    if rank == 0 and not args.quick:
+        import ctypes
+        from paper_1711_00903_b200 import _native
+        bsh = ctypes.c_double()
+        _native.check(_native.lib().hx_measure_smem_bandwidth(
+            ctypes.byref(bsh), torch.cuda.current_stream().cuda_stream))
+        calib = {"b_smem_measured_gb_per_s": bsh.value / 1e9,
+                 "b_smem_paper_ansatz_gb_per_s": hx.shared_bandwidth_ansatz(
+                     148, 32, 4, 1.965) / 1e9,
+                 "note": "measured LDS.64 bandwidth (hx_measure_smem_bandwidth) replaces "
+                         "the paper's B_sh ansatz (PAPER.md:476-487)"}
 
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
@@ -402,6 +488,8 @@ def run_ours(args):
             "clocks": clocks.summary(),
             "cpu_baseline": cpu,
             "per_bp": per_bp,
+            "cg": cg,
+            "calibration": calib,
             "gflop_per_s": hx.flop_model(bp, "fused", DEGREE) * dofs_all / (DEGREE + 1) ** 3
                            / (ms_per_step * 1e-3) / 1e9,
         }

@@ -1,8 +1,9 @@
 // BP1.0 -- mass matvec with de-aliased Gauss quadrature (reference
 // operators.py:274-281):  out = I^T ( GwJ * I q ),  I: GLL(n) -> GL(m).
 //
-// Persistent CTAs over tiles of EPB elements, one 1-D line per thread,
-// per-element tensors in padded shared memory (hx_layouts.h phases X, Y):
+// Persistent CTAs over tiles of EPB elements; a thread owns one 1-D line per
+// stage (or walks over several when the CTA is smaller than the tile's line
+// count); per-element tensors in padded shared memory (hx_layouts.h X, Y):
 //
 //   S1 j-lines (k,i)  n^2 : q (HBM, 8n-byte runs) -> I_s -> X[k][a][i]
 //   S2 i-lines (k,a)  n*m : X -> I_r -> Y[k][a][c]
@@ -45,9 +46,12 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT, HX_MINB_BP1_OF(N))
     bp1_kernel(const __grid_constant__ BP1Params<N> p) {
   using C = Cfg<kBP1, N>;
   constexpr int n = N + 1, m = N + 2, n2 = n * n, n3 = n2 * n, m2 = m * m;
-  constexpr int EPB = C::EPB;
+  constexpr int EPB = C::EPB, NT = C::NT;
   constexpr Lay LX = C::L[0], LY = C::L[1];
   constexpr int EX = C::EBUF[0], EY = C::EBUF[1];
+  // a thread owns one line per stage when NT covers the tile's lines, else
+  // it walks over several (small CTAs: cheap barriers, many CTAs per SM)
+  constexpr bool ONE_C = EPB * m2 <= NT;
   extern __shared__ double smem[];
   double* const X = smem;
   double* const Y = X + EPB * EX;
@@ -63,11 +67,6 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT, HX_MINB_BP1_OF(N))
     prefetch_l2(p.gwj + e0 * fs, ne * fs * sizeof(double));
   }
 
-  // line ownership per stage shape
-  const int el_a = tid / n2, ln_a = tid % n2;  // n^2 lines (S1, S5)
-  const int el_b = tid / (n * m), ln_b = tid % (n * m);  // n*m lines (S2, S4)
-  const int el_c = tid / m2, ln_c = tid % m2;  // m^2 lines (S3)
-
   double en = 0.0;  // this thread's share of <q, A q> (ENERGY)
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t e0 = tile * EPB;
@@ -82,17 +81,22 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT, HX_MINB_BP1_OF(N))
       }
     }
     // GwJ of this thread's S3 k-line, issued early so its latency hides
-    // behind S1 and S2.
+    // behind S1 and S2 (one-line-per-thread shapes only).
     double w[m];
-    if (el_c < ne) {
-      const double* g = p.gwj + (e0 + el_c) * fs + ln_c;
+    if constexpr (ONE_C) {
+      const int el_c = tid / m2, ln_c = tid % m2;
+      if (el_c < ne) {
+        const double* g = p.gwj + (e0 + el_c) * fs + ln_c;
 #pragma unroll
-      for (int c = 0; c < m; ++c) w[c] = g[c * m2];
+        for (int c = 0; c < m; ++c) w[c] = g[c * m2];
+      }
     }
     // ---- S1: j-lines (k, i): interpolate along s
-    if (el_a < ne) {
-      const int k = ln_a / n, i = ln_a % n;
-      const double* src = p.q + (e0 + el_a) * n3 + k * n2 + i;
+    for_lines<EPB * n2, NT>(tid, [&](int g) {
+      const int el = g / n2, ln = g % n2;
+      if (el >= ne) return;
+      const int k = ln / n, i = ln % n;
+      const double* src = p.q + (e0 + el) * n3 + k * n2 + i;
       double x[n], y[m];
       bool bad = false;
 #pragma unroll
@@ -102,68 +106,85 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT, HX_MINB_BP1_OF(N))
       }
       if (bad && p.flag) atomicOr(p.flag, 1);
       fold_apply<m, n, 1>(p.I, x, y);
-      double* dst = X + el_a * EX + k * LX.s0 + i;
+      double* dst = X + el * EX + k * LX.s0 + i;
 #pragma unroll
       for (int t = 0; t < m; ++t) dst[t * LX.s1] = y[t];
-    }
+    });
     __syncthreads();
     // ---- S2: i-lines (k, a): interpolate along r
-    if (el_b < ne) {
-      const int k = ln_b / m, a = ln_b % m;
-      const double* src = X + el_b * EX + k * LX.s0 + a * LX.s1;
+    for_lines<EPB * n * m, NT>(tid, [&](int g) {
+      const int el = g / (n * m), ln = g % (n * m);
+      if (el >= ne) return;
+      const int k = ln / m, a = ln % m;
+      const double* src = X + el * EX + k * LX.s0 + a * LX.s1;
       double x[n], y[m];
 #pragma unroll
       for (int t = 0; t < n; ++t) x[t] = src[t];
       fold_apply<m, n, 1>(p.I, x, y);
-      double* dst = Y + el_b * EY + k * LY.s0 + a * LY.s1;
+      double* dst = Y + el * EY + k * LY.s0 + a * LY.s1;
 #pragma unroll
       for (int t = 0; t < m; ++t) dst[t] = y[t];
-    }
+    });
     __syncthreads();
     // ---- S3: k-lines (a, c): interpolate along t, scale, project along t
-    if (el_c < ne) {
-      const int a = ln_c / m, c = ln_c % m;
-      double* line = Y + el_c * EY + a * LY.s1 + c;
+    for_lines<EPB * m2, NT>(tid, [&](int g) {
+      const int el = g / m2, ln = g % m2;
+      if (el >= ne) return;
+      const int a = ln / m, c = ln % m;
+      double wl[m];
+      if constexpr (ONE_C) {
+#pragma unroll
+        for (int t = 0; t < m; ++t) wl[t] = w[t];
+      } else {
+        const double* gp = p.gwj + (e0 + el) * fs + ln;
+#pragma unroll
+        for (int t = 0; t < m; ++t) wl[t] = gp[t * m2];
+      }
+      double* line = Y + el * EY + a * LY.s1 + c;
       double x[n], y[m];
 #pragma unroll
       for (int t = 0; t < n; ++t) x[t] = line[t * LY.s0];
       fold_apply<m, n, 1>(p.I, x, y);
 #pragma unroll
       for (int t = 0; t < m; ++t) {
-        const double wy = y[t] * w[t];
+        const double wy = y[t] * wl[t];
         if constexpr (ENERGY) en += wy * y[t];  // <q, A q> = sum GwJ (I q)^2
         y[t] = wy;
       }
       fold_apply<n, m, 1>(p.It, y, x);
 #pragma unroll
       for (int t = 0; t < n; ++t) line[t * LY.s0] = x[t];
-    }
+    });
     __syncthreads();
     // ---- S4: i-lines (k, a): project along r
-    if (el_b < ne) {
-      const int k = ln_b / m, a = ln_b % m;
-      const double* src = Y + el_b * EY + k * LY.s0 + a * LY.s1;
+    for_lines<EPB * n * m, NT>(tid, [&](int g) {
+      const int el = g / (n * m), ln = g % (n * m);
+      if (el >= ne) return;
+      const int k = ln / m, a = ln % m;
+      const double* src = Y + el * EY + k * LY.s0 + a * LY.s1;
       double x[m], y[n];
 #pragma unroll
       for (int t = 0; t < m; ++t) x[t] = src[t];
       fold_apply<n, m, 1>(p.It, x, y);
-      double* dst = X + el_b * EX + k * LX.s0 + a * LX.s1;
+      double* dst = X + el * EX + k * LX.s0 + a * LX.s1;
 #pragma unroll
       for (int t = 0; t < n; ++t) dst[t] = y[t];
-    }
+    });
     __syncthreads();
     // ---- S5: j-lines (k, i): project along s and store
-    if (el_a < ne) {
-      const int k = ln_a / n, i = ln_a % n;
-      const double* src = X + el_a * EX + k * LX.s0 + i;
+    for_lines<EPB * n2, NT>(tid, [&](int g) {
+      const int el = g / n2, ln = g % n2;
+      if (el >= ne) return;
+      const int k = ln / n, i = ln % n;
+      const double* src = X + el * EX + k * LX.s0 + i;
       double x[m], y[n];
 #pragma unroll
       for (int t = 0; t < m; ++t) x[t] = src[t * LX.s1];
       fold_apply<n, m, 1>(p.It, x, y);
-      double* dst = p.out + (e0 + el_a) * n3 + k * n2 + i;
+      double* dst = p.out + (e0 + el) * n3 + k * n2 + i;
 #pragma unroll
       for (int t = 0; t < n; ++t) st_stream(dst + t * n, y[t]);
-    }
+    });
     __syncthreads();  // X is rewritten by the next tile's S1
   }
   if constexpr (ENERGY) {

@@ -141,6 +141,17 @@ __device__ __forceinline__ void load_kline(const double* qe, int line, double (&
 // prefetched inputs resident in L2 instead.
 __device__ __forceinline__ void st_stream(double* p, double v) { __stcs(p, v); }
 
+// Run f(line) for this thread's lines of a stage with TOT lines on NT threads
+// (line = tid, tid + NT, ...); a single guarded call when NT >= TOT.
+template <int TOT, int NT, class F>
+__device__ __forceinline__ void for_lines(int tid, F&& f) {
+#pragma unroll
+  for (int it = 0; it < (TOT + NT - 1) / NT; ++it) {
+    const int g = tid + it * NT;
+    if (g < TOT) f(g);
+  }
+}
+
 // Sum of one double per thread over the CTA (result valid in thread 0).
 // `scratch` is shared memory of at least NT/32 doubles that no thread is
 // still reading.

@@ -133,8 +133,17 @@ cudaError_t launch_repack(const hx_plan& P, const double* src, int64_t n_el, dou
 }
 
 // Shared-memory bandwidth probe: every warp streams conflict-free 64-bit
-// loads from a 32 KB smem tile; the accumulated value is written out so the
-// loads cannot be elided.
+// loads (32 consecutive doubles per warp request) from a 32 KB smem tile.
+// The loads are volatile PTX so the compiler cannot merge repeated
+// addresses, and the sum is written out so they cannot be elided.
+__device__ __forceinline__ double lds_volatile(const double* p) {
+  double v;
+  asm volatile("ld.volatile.shared.f64 %0, [%1];"
+               : "=d"(v)
+               : "r"(static_cast<unsigned>(__cvta_generic_to_shared(p))));
+  return v;
+}
+
 __global__ void __launch_bounds__(512) smem_probe_kernel(double* sink, int iters) {
   __shared__ double buf[4096];
   for (int i = threadIdx.x; i < 4096; i += blockDim.x) buf[i] = i * 1e-9;
@@ -145,10 +154,10 @@ __global__ void __launch_bounds__(512) smem_probe_kernel(double* sink, int iters
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int base = ((it * 8 + u) * 128) & 4095;
-      acc0 += buf[(base + lane) & 4095];
-      acc1 += buf[(base + lane + 512) & 4095];
-      acc2 += buf[(base + lane + 1024) & 4095];
-      acc3 += buf[(base + lane + 1536) & 4095];
+      acc0 += lds_volatile(buf + ((base + lane) & 4095));
+      acc1 += lds_volatile(buf + ((base + lane + 1024) & 4095));
+      acc2 += lds_volatile(buf + ((base + lane + 2048) & 4095));
+      acc3 += lds_volatile(buf + ((base + lane + 3072) & 4095));
     }
   }
   if (acc0 + acc1 + acc2 + acc3 == 42.0) sink[blockIdx.x] = acc0;
