@@ -13,8 +13,9 @@ from .mesh import (FACTOR_NAMES, DegenerateGeometryError, GeometricFactors, HexM
 from .operators import (AccessCounters, FieldVector, OperatorInstance, UnsupportedVariantError,
                         apply_bp1, apply_bp3, apply_bp35, apply_device, apply_host,
                         apply_operator, make_operator)
-from .perf import (BENCHMARKS, BP1, BP3, BP35, VARIANTS, TrafficModel, element_counters,
-                   flop_model, roofline_global, roofline_shared, shared_bandwidth_ansatz,
+from .perf import (BENCHMARKS, BP1, BP3, BP35, VARIANTS, RooflinePoint, RooflineSeries,
+                   TrafficModel, element_counters, flop_model, roofline_global,
+                   roofline_series, roofline_shared, scratch_traffic, shared_bandwidth_ansatz,
                    traffic)
 from .quadrature import (QuadratureRule, check_rule, gl_rule, gll_rule, lagrange_deriv,
                          lagrange_eval, legendre_and_derivative)

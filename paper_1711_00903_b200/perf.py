@@ -9,7 +9,7 @@ exactly linear in the element count, so they are charged once per element
 and scaled, never by touching the data.
 """
 
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
 BP1 = "BP1.0"
 BP35 = "BP3.5"
@@ -100,6 +100,57 @@ def roofline_shared(b_sh, flops, s_r, s_w):
     if s_r + s_w <= 0:
         raise ValueError("scratch traffic must be positive")
     return b_sh * flops / (s_r + s_w)
+
+
+@dataclass(frozen=True)
+class RooflinePoint:
+    degree: int
+    flops: int
+    bytes_moved: int
+    r_global: float
+    r_shared: float = None
+
+    @property
+    def bound(self):
+        return self.r_global if self.r_shared is None else min(self.r_global, self.r_shared)
+
+
+@dataclass(frozen=True)
+class RooflineSeries:
+    bp: str
+    variant: str
+    n_el: int
+    bandwidth: float
+    shared_bandwidth: float
+    points: list = field(default_factory=list)
+
+
+def scratch_traffic(bp, variant, degree):
+    """Per-element scratch bytes (reads, writes) of one apply -- reference
+    perf.py:172-178 re-runs a one-element apply to read its counters; the
+    counters are value-independent, so they are charged analytically here."""
+    c = element_counters(bp, variant, degree)
+    return c["scratch_reads"], c["scratch_writes"]
+
+
+def roofline_series(bp, degrees, n_el, b_gl, variant="fused", b_sh=None):
+    """Model series across degrees (reference perf.py:181-201): the global
+    roofline from Table 1 and, for the interpolation-bearing benchmarks, the
+    scratch roofline from the modelled scratch traffic.  Feed it the
+    measured B_copy and B_smem of the device (bench.py's calibration)."""
+    with_shared = b_sh is not None and bp != BP35
+    points = []
+    for degree in degrees:
+        t = traffic(bp, degree, n_el)
+        flops = flop_model(bp, variant, degree) * n_el
+        r_gl = roofline_global(b_gl, flops, 8 * t.reads_doubles * n_el,
+                               8 * t.writes_doubles * n_el)
+        r_sh = None
+        if with_shared:
+            s_r, s_w = scratch_traffic(bp, variant, degree)
+            r_sh = roofline_shared(b_sh, flop_model(bp, variant, degree), s_r, s_w)
+        points.append(RooflinePoint(degree, flops, t.bytes_per_element * n_el, r_gl, r_sh))
+    return RooflineSeries(bp, variant, n_el, b_gl, b_sh if with_shared else None, points)
 
 
 # ---------------------------------------------------------------------------

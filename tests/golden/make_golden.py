@@ -102,6 +102,14 @@ def main():
              for d in range(1, 16)], dtype=np.int64)
         g[f"flops_{tag(bp)}"] = np.array([perf.flop_model(bp, "fused", d)
                                           for d in range(1, 16)], dtype=np.int64)
+        for variant in ("fused", "symfused", "baseline"):
+            if variant == "symfused" and bp == BP35:
+                continue
+            ser = perf.roofline_series(bp, range(1, 16), 512, 549e9, variant=variant,
+                                       b_sh=perf.shared_bandwidth_ansatz())
+            g[f"roofline_{tag(bp)}_{variant}"] = np.array(
+                [[p.r_global, np.nan if p.r_shared is None else p.r_shared]
+                 for p in ser.points])
     for n in range(1, 21):
         r = gl_rule(n)
         g[f"gl{n}"] = np.stack([r.nodes, r.weights])

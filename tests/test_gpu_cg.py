@@ -92,3 +92,20 @@ def test_cg_bitwise_reproducible(mesh3):
     x2 = cg_iterations(op, b, 25, w)
     torch.cuda.synchronize()
     assert torch.equal(x1, x2)
+
+
+def test_report_bench_schema():
+    """Reporting integration: the reference's `hexbench bench` run keys
+    (cli.py:262-284) filled from device timings."""
+    from paper_1711_00903_b200.report import bench_runs
+
+    runs = bench_runs([hx.BP1, hx.BP35], [2], 3, repeats=3)
+    ref_keys = {"bp", "degree", "variant", "elements", "wall_time_mean_s", "wall_time_median_s",
+                "achieved_flops_per_s", "flops", "counted_global_bytes",
+                "counted_scratch_bytes", "model_bytes", "syncs", "bandwidth_bytes_per_s",
+                "r_global_flops_per_s"}
+    for r in runs:
+        assert ref_keys <= set(r)
+        assert r["counted_global_bytes"] == r["model_bytes"]
+        assert r["wall_time_median_s"] > 0 and r["gdof_per_s"] > 0
+    assert "r_shared_flops_per_s" in runs[0] and "r_shared_flops_per_s" not in runs[1]
