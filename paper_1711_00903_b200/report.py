@@ -92,7 +92,7 @@ def bench_runs(bps, degrees, side, variant="fused", lam=1.0, repeats=10, seed=0,
             counters = AccessCounters()
             _charge(op, counters)
             model = perf.traffic(bp, deg, mesh.n_el)
-            b_gl = bandwidth if bandwidth is not None else \\
+            b_gl = bandwidth if bandwidth is not None else \
                 device_copy_bandwidth(model.copy_equivalent_bytes)
             med = statistics.median(times)
             nbytes = model.bytes_per_element * mesh.n_el

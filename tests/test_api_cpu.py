@@ -89,3 +89,21 @@ def test_mesh_helpers():
         hx.trilinear_jacobian(flat, 0.0, 0.0, 0.0)
     with pytest.raises(ValueError):
         hx.build_cube_mesh(0, 2.0)
+
+
+def test_every_module_imports():
+    """Every product module, tool and entry point at least compiles and the
+    package modules import without a GPU (GPU-only tests must not be the first
+    place a syntax error shows up)."""
+    import importlib
+    import pathlib
+
+    root = pathlib.Path(__file__).resolve().parents[1]
+    for path in [root / "bench.py", root / "__graft_entry__.py",
+                 *sorted((root / "paper_1711_00903_b200").glob("*.py")),
+                 *sorted((root / "tools").glob("*.py")),
+                 *sorted((root / "oracle").glob("*.py"))]:
+        compile(path.read_text(), str(path), "exec")
+    for path in sorted((root / "paper_1711_00903_b200").glob("*.py")):
+        if path.stem != "__init__":
+            importlib.import_module(f"paper_1711_00903_b200.{path.stem}")
