@@ -95,6 +95,17 @@ int hx_apply_host(const hx_plan* plan, const double* q_host, const double* facto
                   double* out_host, int64_t n_el, int64_t chunk_el, void* work,
                   int* status_flag, void* stream);
 
+/* Element helpers, batched: replace interpolate_to_gl / project_to_gll
+ * (operators.py:352-364), which act on one (n,n,n) / (m,m,m) element tensor.
+ * `interp` is the HOST m x n row-major GLL->GL matrix (reference_ops.py:39-44,
+ * m = degree+2, n = degree+1); `src`/`dst` are device arrays of n_el element
+ * tensors, (k,j,i) point order:
+ *   project = 0: dst (n_el, m^3) = I (x) I (x) I  src (n_el, n^3)
+ *   project = 1: dst (n_el, n^3) = I^T (x) I^T (x) I^T  src (n_el, m^3)
+ * status_flag as in hx_apply (non-finite src).  Asynchronous on `stream`.    */
+int hx_interp_elements(int degree, const double* interp, int project, const double* src,
+                       double* dst, int64_t n_el, int* status_flag, void* stream);
+
 /* apply + <q, A q>: as hx_apply, and *energy (device double) receives
  * <q, A q>, evaluated inside the kernel from its quadrature-point values
  * (grad q . G grad q + lam GwJ q^2; GwJ (I q)^2 for BP1.0) -- no extra pass

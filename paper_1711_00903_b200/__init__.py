@@ -12,7 +12,8 @@ from .mesh import (FACTOR_NAMES, DegenerateGeometryError, GeometricFactors, HexM
                    trilinear_map)
 from .operators import (AccessCounters, FieldVector, OperatorInstance, UnsupportedVariantError,
                         apply_bp1, apply_bp3, apply_bp35, apply_device, apply_host,
-                        apply_operator, make_operator)
+                        apply_operator, interpolate_to_gl, make_operator,
+                        project_to_gll)
 from .perf import (BENCHMARKS, BP1, BP3, BP35, VARIANTS, RooflinePoint, RooflineSeries,
                    TrafficModel, element_counters, flop_model, roofline_global,
                    roofline_series, roofline_shared, scratch_traffic, shared_bandwidth_ansatz,

@@ -41,7 +41,7 @@ struct BP1Params {
   double* energy;  // per-CTA partials of <q, A q> (ENERGY instantiation only)
 };
 
-template <int N, bool ENERGY>
+template <int N, bool ENERGY, bool STAGE>
 __global__ void __launch_bounds__(Cfg<kBP1, N>::NT, HX_MINB_BP1_OF(N))
     bp1_kernel(const __grid_constant__ BP1Params<N> p) {
   using C = Cfg<kBP1, N>;
@@ -49,21 +49,51 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT, HX_MINB_BP1_OF(N))
   constexpr int EPB = C::EPB, NT = C::NT;
   constexpr Lay LX = C::L[0], LY = C::L[1];
   constexpr int EX = C::EBUF[0], EY = C::EBUF[1];
+  // lane orders of the j-line (S1, S5) and i-line (S2, S4) stages: k fastest
+  constexpr bool JKF = C::ORD & 1, IKF = C::ORD & 2;
   // a thread owns one line per stage when NT covers the tile's lines, else
   // it walks over several (small CTAs: cheap barriers, many CTAs per SM)
   constexpr bool ONE_C = EPB * m2 <= NT;
+  // QS > 0: the q tile is staged in shared memory by the bulk-copy engine
+  // one tile ahead (k-slabs of n*n doubles at stride QS), so S1 never waits
+  // on HBM; the q L2 prefetch is then not needed.
+  constexpr int QS = C::QS;
+  constexpr bool QST = STAGE && QS > 0;
   extern __shared__ double smem[];
-  double* const X = smem;
+  uint64_t* const qbar = reinterpret_cast<uint64_t*>(smem);
+  double* const QT = smem + (QST ? 2 : 0);
+  double* const X = QT + (QST ? EPB * n * QS : 0);
   double* const Y = X + EPB * EX;
 
   const int tid = threadIdx.x;
   const int64_t ntiles = (p.n_el + EPB - 1) / EPB;
   const int64_t fs = p.fac_estride;
 
+  // warp 0 stages tile `t`'s q: lane 0 arms the barrier with the byte count,
+  // then the lanes issue one k-slab copy each
+  auto stage_q = [&](int64_t t) {
+    if constexpr (QST) {
+      const int64_t f0 = t * EPB;
+      const int nn = int(min64(EPB, p.n_el - f0));
+      const int lane = tid & 31;
+      if (lane == 0) mbar_arrive_expect_tx(qbar, unsigned(nn * n3 * sizeof(double)));
+      __syncwarp();
+      const uint64_t pol = l2_evict_first_policy();
+      for (int s = lane; s < nn * n; s += 32)
+        bulk_g2s(QT + s * QS, p.q + f0 * n3 + int64_t(s) * n2, n2 * sizeof(double), qbar, pol);
+    }
+  };
+  if constexpr (QST) {
+    if (tid == 0) mbar_init(qbar, 1);
+    __syncthreads();
+    if (tid < 32 && blockIdx.x < ntiles) stage_q(blockIdx.x);
+  }
+  unsigned qphase = 0;
+
   if (tid == 0 && blockIdx.x < ntiles) {
     const int64_t e0 = int64_t(blockIdx.x) * EPB;
     const int64_t ne = min64(EPB, p.n_el - e0);
-    prefetch_l2(p.q + e0 * n3, ne * n3 * sizeof(double));
+    if constexpr (!QST) prefetch_l2(p.q + e0 * n3, ne * n3 * sizeof(double));
     prefetch_l2(p.gwj + e0 * fs, ne * fs * sizeof(double));
   }
 
@@ -76,7 +106,7 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT, HX_MINB_BP1_OF(N))
       if (nt < ntiles) {
         const int64_t f0 = nt * EPB;
         const int64_t nn = min64(EPB, p.n_el - f0);
-        prefetch_l2(p.q + f0 * n3, nn * n3 * sizeof(double));
+        if constexpr (!QST) prefetch_l2(p.q + f0 * n3, nn * n3 * sizeof(double));
         prefetch_l2(p.gwj + f0 * fs, nn * fs * sizeof(double));
       }
     }
@@ -92,11 +122,16 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT, HX_MINB_BP1_OF(N))
       }
     }
     // ---- S1: j-lines (k, i): interpolate along s
+    if constexpr (QST) {
+      mbar_wait(qbar, qphase);
+      qphase ^= 1u;
+    }
     for_lines<EPB * n2, NT>(tid, [&](int g) {
       const int el = g / n2, ln = g % n2;
       if (el >= ne) return;
-      const int k = ln / n, i = ln % n;
-      const double* src = p.q + (e0 + el) * n3 + k * n2 + i;
+      int k, i;
+      line_coords<n, n, JKF>(ln, k, i);
+      const double* src = QST ? QT + (el * n + k) * QS + i : p.q + (e0 + el) * n3 + k * n2 + i;
       double x[n], y[m];
       bool bad = false;
 #pragma unroll
@@ -111,11 +146,19 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT, HX_MINB_BP1_OF(N))
       for (int t = 0; t < m; ++t) dst[t * LX.s1] = y[t];
     });
     __syncthreads();
+    if constexpr (QST) {
+      // the staged q has been consumed: fetch the next tile's into it
+      if (tid < 32 && tile + gridDim.x < ntiles) {
+        fence_proxy_async_smem();
+        stage_q(tile + gridDim.x);
+      }
+    }
     // ---- S2: i-lines (k, a): interpolate along r
     for_lines<EPB * n * m, NT>(tid, [&](int g) {
       const int el = g / (n * m), ln = g % (n * m);
       if (el >= ne) return;
-      const int k = ln / m, a = ln % m;
+      int k, a;
+      line_coords<n, m, IKF>(ln, k, a);
       const double* src = X + el * EX + k * LX.s0 + a * LX.s1;
       double x[n], y[m];
 #pragma unroll
@@ -160,7 +203,8 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT, HX_MINB_BP1_OF(N))
     for_lines<EPB * n * m, NT>(tid, [&](int g) {
       const int el = g / (n * m), ln = g % (n * m);
       if (el >= ne) return;
-      const int k = ln / m, a = ln % m;
+      int k, a;
+      line_coords<n, m, IKF>(ln, k, a);
       const double* src = Y + el * EY + k * LY.s0 + a * LY.s1;
       double x[m], y[n];
 #pragma unroll
@@ -175,7 +219,8 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT, HX_MINB_BP1_OF(N))
     for_lines<EPB * n2, NT>(tid, [&](int g) {
       const int el = g / n2, ln = g % n2;
       if (el >= ne) return;
-      const int k = ln / n, i = ln % n;
+      int k, i;
+      line_coords<n, n, JKF>(ln, k, i);
       const double* src = X + el * EX + k * LX.s0 + i;
       double x[m], y[n];
 #pragma unroll
@@ -193,24 +238,34 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT, HX_MINB_BP1_OF(N))
   }
 }
 
-template <int N, bool E, class Prm>
+template <int N, bool E, bool STAGE, class Prm>
 static cudaError_t launch_t(const Prm& prm, int64_t n_el, cudaStream_t s) {
   using C = Cfg<kBP1, N>;
   constexpr int smem = smem_doubles<kBP1, N>() * int(sizeof(double));
   static int blocks_per_sm = -1;
   if (blocks_per_sm < 0) {
-    cudaError_t err = cudaFuncSetAttribute(bp1_kernel<N, E>,
+    cudaError_t err = cudaFuncSetAttribute(bp1_kernel<N, E, STAGE>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (err != cudaSuccess) return err;
-    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, bp1_kernel<N, E>, C::NT,
-                                                        smem);
+    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, bp1_kernel<N, E, STAGE>,
+                                                        C::NT, smem);
     if (err != cudaSuccess) return err;
     if (blocks_per_sm < 1) blocks_per_sm = 1;
   }
   const int64_t ntiles = (n_el + C::EPB - 1) / C::EPB;
   const int64_t grid = min64(ntiles, int64_t(blocks_per_sm) * sm_count());
-  bp1_kernel<N, E><<<unsigned(grid), C::NT, smem, s>>>(prm);
+  bp1_kernel<N, E, STAGE><<<unsigned(grid), C::NT, smem, s>>>(prm);
   return cudaGetLastError();
+}
+
+// The staged shape needs 16-byte aligned q (the bulk engine's rule); a q
+// view that is only 8-byte aligned takes the unstaged instantiation.
+template <int N, bool E, class Prm>
+static cudaError_t launch_s(const Prm& prm, int64_t n_el, cudaStream_t s) {
+  if constexpr (Cfg<kBP1, N>::QS > 0) {
+    if ((reinterpret_cast<uintptr_t>(prm.q) & 15) == 0) return launch_t<N, E, true>(prm, n_el, s);
+  }
+  return launch_t<N, E, false>(prm, n_el, s);
 }
 
 template <int N>
@@ -231,7 +286,7 @@ static cudaError_t launch_n(const hx_plan& P, const double* q, const double* fac
   prm.fac_estride = P.elem_stride;
   prm.flag = flag;
   prm.energy = energy;
-  return energy ? launch_t<N, true>(prm, n_el, s) : launch_t<N, false>(prm, n_el, s);
+  return energy ? launch_s<N, true>(prm, n_el, s) : launch_s<N, false>(prm, n_el, s);
 }
 
 cudaError_t launch_bp1(const hx_plan& P, const double* q, const double* fac, double* out,

@@ -1,5 +1,6 @@
 // C ABI entry points (include/hexbench_b200.h).  Thin: validate, dispatch to
 // the per-operator launchers, translate CUDA errors into HX_ECUDA.
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -54,6 +55,23 @@ static cudaError_t launch(const hx_plan& P, const double* q, const double* fac, 
   }
 }
 
+// The kernels apply the 1-D matrices in even/odd folded form, which is exact
+// only for centro-symmetric (sign +1: I, I^T) or centro-antisymmetric (sign
+// -1: D, D~) matrices -- true of the reference's (reference_ops.py:42-44).
+// Anything else is rejected rather than silently mis-applied.
+static bool centro_ok(const double* M, int R, int C, double sign) {
+  double scale = 0.0;
+  for (int a = 0; a < R * C; ++a) {
+    if (!std::isfinite(M[a])) return false;
+    scale = std::fmax(scale, std::fabs(M[a]));
+  }
+  for (int a = 0; a < R; ++a)
+    for (int b = 0; b < C; ++b)
+      if (std::fabs(M[a * C + b] - sign * M[(R - 1 - a) * C + (C - 1 - b)]) > 1e-12 * scale)
+        return false;
+  return true;
+}
+
 static thread_local char g_last_cuda[256];
 
 static int cuda_status(cudaError_t err) {
@@ -79,6 +97,11 @@ int hx_plan_create(int bp, int degree, double lam, const double* interp, const d
   if (!nodes || !weights) return HX_EINVAL;
   if (bp != HX_BP35 && !interp) return HX_EINVAL;
   if (bp != HX_BP1 && !diff) return HX_EINVAL;
+  {
+    const int n = degree + 1, m = degree + 2, q = bp == HX_BP35 ? n : m;
+    if (interp && bp != HX_BP35 && !centro_ok(interp, m, n, 1.0)) return HX_EINVAL;
+    if (diff && bp != HX_BP1 && !centro_ok(diff, q, q, -1.0)) return HX_EINVAL;
+  }
   hx_plan* P = new (std::nothrow) hx_plan();
   if (!P) return HX_ENOMEM;
   P->bp = bp;
@@ -145,7 +168,23 @@ int hx_apply(const hx_plan* P, const double* q, const double* factors, double* o
              int64_t n_el, int* flag, void* stream) {
   if (!P || n_el < 0) return HX_EINVAL;
   if (n_el > 0 && (!q || !factors || !out)) return HX_EINVAL;
+  // doubles must be naturally aligned (16-byte alignment is not required)
+  if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(factors) |
+       reinterpret_cast<uintptr_t>(out)) & 7)
+    return HX_EINVAL;
   return cuda_status(launch(*P, q, factors, out, n_el, flag, static_cast<cudaStream_t>(stream)));
+}
+
+int hx_interp_elements(int degree, const double* interp, int project, const double* src,
+                       double* dst, int64_t n_el, int* flag, void* stream) {
+  if (degree < 1 || degree > 15 || n_el < 0 || !interp) return HX_EINVAL;
+  if (project != 0 && project != 1) return HX_EINVAL;
+  if (n_el == 0) return HX_OK;
+  if (!src || !dst) return HX_EINVAL;
+  if ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 7) return HX_EINVAL;
+  if (!centro_ok(interp, degree + 2, degree + 1, 1.0)) return HX_EINVAL;
+  return cuda_status(launch_interp(degree, interp, project, src, dst, n_el, flag,
+                                   static_cast<cudaStream_t>(stream)));
 }
 
 int64_t hx_apply_host_workspace(const hx_plan* P, int64_t chunk_el) {

@@ -112,6 +112,61 @@ __device__ __forceinline__ void prefetch_l2(const void* ptr, size_t bytes) {
   }
 }
 
+// ---- bulk-copy (TMA engine, non-tensor) staging with an mbarrier ----------
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count)
+               : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+// Arm the barrier's current phase with this thread's arrival and `bytes` of
+// expected bulk-copy transactions.
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      " .reg .pred p;\n"
+      "HX_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra HX_WAIT_%=;\n"
+      "}\n" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// Generic-proxy accesses to shared memory made before this (and ordered by a
+// barrier) are ordered before later async-proxy (bulk copy) writes.
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// HBM -> shared bulk copy of `bytes` (multiple of 16, both addresses 16-byte
+// aligned) completing as transactions on `bar`.  The source is streamed once:
+// L2 evict-first so it does not displace data still to be read.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(policy)
+      : "memory");
+}
+
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
 __host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
 
 __device__ __forceinline__ bool nonfinite(double v) {
@@ -152,6 +207,21 @@ __device__ __forceinline__ void for_lines(int tid, F&& f) {
   }
 }
 
+// Coordinates (first, second) of line `ln` of a stage whose lines form an
+// (A x B) grid: row-major (second fastest across lanes) or, with FIRST_FAST,
+// first fastest.  The generated ORD flags pick the order per stage so that
+// the lanes of a half-warp hit distinct shared-memory banks.
+template <int A, int B, bool FIRST_FAST>
+__device__ __forceinline__ void line_coords(int ln, int& first, int& second) {
+  if constexpr (FIRST_FAST) {
+    first = ln % A;
+    second = ln / A;
+  } else {
+    first = ln / B;
+    second = ln % B;
+  }
+}
+
 // Sum of one double per thread over the CTA (result valid in thread 0).
 // `scratch` is shared memory of at least NT/32 doubles that no thread is
 // still reading.
@@ -168,12 +238,17 @@ __device__ __forceinline__ double block_sum(double v, double* scratch) {
   return s;
 }
 
+// Shared memory per CTA in doubles: the per-element tensor buffers, plus for
+// the TMA q-staged BP1.0 shape the staged q tile and 2 doubles (16 bytes,
+// keeps the staging 16-byte aligned) holding its mbarrier.
 template <int BP, int N>
 constexpr int smem_doubles() {
   using C = Cfg<BP, N>;
   int s = 0;
   for (int b = 0; b < int(sizeof(C::EBUF) / sizeof(int)); ++b) s += C::EBUF[b];
-  return s * C::EPB;
+  s *= C::EPB;
+  if (C::QS > 0) s += 2 + C::EPB * (N + 1) * C::QS;
+  return s;
 }
 
 }  // namespace hx

@@ -323,3 +323,64 @@ def apply_bp3(op, q, counters=None, threads=1):
     if op.bp != BP3:
         raise ValueError("operator is not BP3.0")
     return apply_operator(op, q, counters, threads)
+
+
+def _interp_entries(interp):
+    mat = interp.entries if hasattr(interp, "entries") else np.asarray(interp, dtype=float)
+    mat = np.ascontiguousarray(mat, dtype=np.float64)
+    if mat.ndim != 2 or mat.shape[0] != mat.shape[1] + 1:
+        raise ValueError("interp must be an (N+2) x (N+1) GLL -> GL matrix")
+    check_degree(mat.shape[1] - 1)
+    return mat
+
+
+def _interp_elements(x, interp, project):
+    """Shared body of interpolate_to_gl / project_to_gll: one batched kernel
+    launch (``hx_interp_elements``) over every element tensor in ``x``."""
+    import torch
+
+    mat = _interp_entries(interp)
+    m, n = mat.shape
+    src_n, dst_n = (m, n) if project else (n, m)
+    on_dev = _is_torch(x)
+    shape = tuple(x.shape)
+    if len(shape) < 3 or shape[-3:] != (src_n,) * 3:
+        raise ValueError(
+            f"expected element tensors of shape (..., {src_n}, {src_n}, {src_n}), got {shape}")
+    batch = shape[:-3]
+    n_el = int(np.prod(batch)) if batch else 1
+    if on_dev:
+        if not x.is_cuda:
+            raise ValueError("torch tensors must live on a CUDA device")
+        dev = x.device
+        src = x.to(torch.float64).contiguous().view(n_el, src_n ** 3)
+    else:
+        dev = torch.device("cuda", torch.cuda.current_device())
+        src = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64).reshape(
+            n_el, src_n ** 3)).to(dev)
+    with torch.cuda.device(dev):
+        dst = torch.empty((n_el, dst_n ** 3), dtype=torch.float64, device=dev)
+        flag = torch.zeros(1, dtype=torch.int32, device=dev)
+        _native.check(_native.lib().hx_interp_elements(
+            n - 1, _native.ptr(mat), int(project), _native.ptr(src), _native.ptr(dst), n_el,
+            _native.ptr(flag), _stream(dev)), "hx_interp_elements")
+        if int(flag.item()) & _native.HX_FLAG_NONFINITE:
+            raise ValueError("element tensor contains non-finite values")
+    dst = dst.view(*batch, dst_n, dst_n, dst_n)
+    return dst if on_dev else dst.cpu().numpy()
+
+
+def interpolate_to_gl(q_e, interp):
+    """Pure interpolation of element tensors from GLL to GL nodes (reference
+    operators.py:352-356): ``(..., n, n, n) -> (..., m, m, m)``, contracting
+    axes 1, 2, 0 of each element with ``interp`` (an OperatorMatrix or an
+    (N+2) x (N+1) array).  numpy in -> numpy out (through the device);
+    a torch CUDA tensor stays on its device.  Any number of leading batch
+    axes: one kernel launch for all of them."""
+    return _interp_elements(q_e, interp, project=False)
+
+
+def project_to_gll(t_e, interp):
+    """Transpose interpolation of element tensors from GL back to GLL
+    (reference operators.py:359-364): ``(..., m, m, m) -> (..., n, n, n)``."""
+    return _interp_elements(t_e, interp, project=True)

@@ -12,6 +12,8 @@ Contents (keys are prefixed ``{bp}_N{deg}_``):
   interp / diff / nodes / weights : the reference 1-D matrices and rule
   factors  : reference geometric_factors (full for N<=4, element 0 otherwise)
   q, out_lam{L} : FieldVector.random input and reference apply_operator output
+plus ``helper_N{deg}_{q,gl,t,gll}`` (reference interpolate_to_gl / project_to_gll
+on three random element tensors),
 plus ``counters_{bp}_{variant}_N{deg}`` (one-element counter values, lam=1),
 ``traffic`` / ``flops`` tables and quadrature rules.
 """
@@ -27,7 +29,9 @@ sys.path.insert(0, REF)
 from hexbench import dense, perf  # noqa: E402
 from hexbench.mesh import build_cube_mesh, perturb_mesh  # noqa: E402
 from hexbench.operators import (BENCHMARKS, BP1, BP3, BP35, AccessCounters,  # noqa: E402
-                                FieldVector, apply_operator, make_operator)
+                                FieldVector, apply_operator, interpolate_to_gl,
+                                make_operator, project_to_gll)
+from hexbench.reference_ops import interp_matrix  # noqa: E402
 from hexbench.quadrature import gl_rule, gll_rule  # noqa: E402
 
 OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden.npz")
@@ -110,6 +114,17 @@ def main():
             g[f"roofline_{tag(bp)}_{variant}"] = np.array(
                 [[p.r_global, np.nan if p.r_shared is None else p.r_shared]
                  for p in ser.points])
+    # element helpers (operators.py:352-364): 3 random element tensors per degree
+    rng = np.random.default_rng(2024)
+    for deg in (1, 2, 3, 5, 7, 8, 15):
+        n, m = deg + 1, deg + 2
+        mat = interp_matrix(deg)
+        q = rng.standard_normal((3, n, n, n))
+        t = rng.standard_normal((3, m, m, m))
+        g[f"helper_N{deg}_q"] = q
+        g[f"helper_N{deg}_gl"] = np.stack([interpolate_to_gl(x, mat) for x in q])
+        g[f"helper_N{deg}_t"] = t
+        g[f"helper_N{deg}_gll"] = np.stack([project_to_gll(x, mat) for x in t])
     for n in range(1, 21):
         r = gl_rule(n)
         g[f"gl{n}"] = np.stack([r.nodes, r.weights])

@@ -107,3 +107,15 @@ def test_every_module_imports():
     for path in sorted((root / "paper_1711_00903_b200").glob("*.py")):
         if path.stem != "__init__":
             importlib.import_module(f"paper_1711_00903_b200.{path.stem}")
+
+
+def test_element_helper_validation_before_device():
+    """interpolate_to_gl / project_to_gll reject bad shapes / matrices on the
+    host (ValueError, like the reference's contract_dim) before any launch."""
+    mat = hx.interp_matrix(3)
+    with pytest.raises(ValueError):
+        hx.interpolate_to_gl(np.zeros((5, 5, 5)), mat)
+    with pytest.raises(ValueError):
+        hx.project_to_gll(np.zeros((4, 4, 4)), mat)
+    with pytest.raises(ValueError):
+        hx.interpolate_to_gl(np.zeros((4, 4, 4)), np.zeros((4, 4)))

@@ -12,7 +12,13 @@ distinct 8-byte words that fall in the same 8-byte bank pair (word mod 16).
 
 Patterns: 0 = k-lines (lanes enumerate (j, i)), 1 = j-lines (lanes (k, i)),
 2 = i-lines (lanes (k, j)); consecutive threads own consecutive lines, and
-the lines of EPB elements are laid end to end.
+the lines of EPB elements are laid end to end.  Patterns 3, 4, 5 are the same
+lines with the lane enumeration transposed (the first coordinate fastest):
+3 = k-lines over (i, j) with j fastest, 4 = j-lines with k fastest, 5 = i-lines
+with k fastest.  BP1.0 picks its j-line / i-line lane orders jointly with the
+strides (``ORD``): with one order per pattern no padding can make both the
+(k,i) j-lines and the (k,a) i-lines of X conflict-free (ncu r08: S2/S4 paid
+1.86x wavefronts), with k fastest in both it can.
 """
 
 import sys
@@ -23,7 +29,7 @@ TARGET_THREADS = 256
 
 def lines(d, pat):
     d0, d1, d2 = d
-    return {0: (d1 * d2, d0), 1: (d0 * d2, d1), 2: (d0 * d1, d2)}[pat]
+    return {0: (d1 * d2, d0), 1: (d0 * d2, d1), 2: (d0 * d1, d2)}[pat % 3]
 
 
 def addr(d, s0, s1, pat, l, t):
@@ -34,7 +40,16 @@ def addr(d, s0, s1, pat, l, t):
     if pat == 1:
         k, i = divmod(l, d2)
         return k * s0 + t * s1 + i
-    k, j = divmod(l, d1)
+    if pat == 2:
+        k, j = divmod(l, d1)
+        return k * s0 + j * s1 + t
+    if pat == 3:
+        i, j = divmod(l, d1)
+        return t * s0 + j * s1 + i
+    if pat == 4:
+        i, k = divmod(l, d0)
+        return k * s0 + t * s1 + i
+    j, k = divmod(l, d0)
     return k * s0 + j * s1 + t
 
 
@@ -71,19 +86,39 @@ def best_layout(d, pats):
     return best[1], best[2]
 
 
-def phases(bp, n, m):
+def phases(bp, n, m, ord_=0):
     """(buffer id, dims, patterns) for every tensor phase of a kernel."""
     if bp == BP35:
         return [(0, (n, n, n), (0, 1, 2)), (1, (n, n, n), (0, 2)),
                 (2, (n, n, n), (0, 1))]
     if bp == BP1:
-        return [(0, (n, m, n), (1, 2)), (1, (n, m, m), (0, 2))]
+        # ord bit 0: j-lines k-fastest (4 instead of 1); bit 1: i-lines (5 for 2)
+        pj = 4 if ord_ & 1 else 1
+        pi = 5 if ord_ & 2 else 2
+        return [(0, (n, m, n), (pj, pi)), (1, (n, m, m), (0, pi))]
     return [(0, (n, m, n), (1, 2)), (0, (m, m, m), (0, 2)),
             (1, (n, m, m), (0, 2)), (1, (m, m, m), (0, 1)),
             (2, (m, m, m), (0, 1, 2)), (2, (n, m, m), (0, 2))]
 
 
-def plan(bp, deg, target=TARGET_THREADS):
+def q_stage_stride(n, ord_=0):
+    """Slab stride (doubles) of BP1.0's TMA-staged q tile: every k-slab
+    (n*n doubles, contiguous in HBM) is one bulk copy, so rows stay dense
+    (s1 = n) and only the slab stride is free; it must keep 16-byte alignment
+    (even) and S1 reads j-lines (pattern 1).  0 when n*n*8 is not a multiple
+    of 16 (odd n): the bulk engine needs 16-byte sizes and addresses."""
+    if n % 2:
+        return 0
+    d = (n, n, n)
+    best = None
+    for s0 in range(n * n, n * n + 16, 2):
+        c = cost(d, s0, n, (4 if ord_ & 1 else 1,), 1, 0)
+        if best is None or c < best[0]:
+            best = (c, s0)
+    return best[1]
+
+
+def plan(bp, deg, target=TARGET_THREADS, qstage=False):
     n, m = deg + 1, deg + 2
     lmax = n * n if bp == BP35 else m * m
     epb = max(1, target // lmax)
@@ -92,14 +127,22 @@ def plan(bp, deg, target=TARGET_THREADS):
         # BP1.0 only: a CTA smaller than one element's line count walks over
         # the lines (for_lines); one element per tile
         nt = max(32, -(-target // 32) * 32)
-    ph = phases(bp, n, m)
-    lays = [best_layout(d, pats) for _, d, pats in ph]
+    ords = (0, 1, 2, 3) if bp == BP1 else (0,)
+    best = None
+    for o in ords:  # BP1.0: lane orders chosen jointly with the strides
+        ph_o = phases(bp, n, m, o)
+        lays_o = [best_layout(d, pats) for _, d, pats in ph_o]
+        c = sum(cost(d, s0, s1, pats, 1, 0) for (_, d, pats), (s0, s1) in zip(ph_o, lays_o))
+        if best is None or c < best[0]:
+            best = (c, o, ph_o, lays_o)
+    _, ord_, ph, lays = best
     nbuf = 1 + max(b for b, _, _ in ph)
     base = [0] * nbuf
     for (b, d, _), (s0, _) in zip(ph, lays):
         base[b] = max(base[b], d[0] * s0)
+    qs = q_stage_stride(n, ord_) if (bp == BP1 and qstage) else 0
     # keep the tile inside the 227 KB shared-memory limit
-    while epb > 1 and epb * (sum(base) + 16 * nbuf) * 8 > 227 * 1024:
+    while epb > 1 and epb * (sum(base) + 16 * nbuf + n * qs) * 8 > 227 * 1024:
         epb -= 1
         nt = -(-epb * lmax // 32) * 32
     ebufs = []
@@ -111,7 +154,7 @@ def plan(bp, deg, target=TARGET_THREADS):
             if best is None or c < best[0]:
                 best = (c, eb)
         ebufs.append(best[1])
-    return n, m, epb, nt, ph, lays, ebufs
+    return n, m, epb, nt, ph, lays, ebufs, qs, ord_
 
 
 def min_blocks(bp, deg):
@@ -126,7 +169,7 @@ def min_blocks(bp, deg):
 
 
 def main(path, policy=None, verbose=False):
-    """policy: {(bp, deg): (target_threads, min_blocks)}; defaults otherwise."""
+    """policy: {(bp, deg): (target_threads, min_blocks, qstage)}; defaults otherwise."""
     policy = policy or {}
     out = ["// Generated by tools/gen_layouts.py -- do not edit by hand.",
            "// Shared-memory strides per (kernel, degree): see that script for the",
@@ -136,10 +179,13 @@ def main(path, policy=None, verbose=False):
            "template <int BP, int N> struct Cfg;", ""]
     for bp in (BP1, BP35, BP3):
         for deg in range(1, 16):
-            target, minb = policy.get((bp, deg), (TARGET_THREADS, min_blocks(bp, deg)))
-            n, m, epb, nt, ph, lays, ebufs = plan(bp, deg, target)
+            target, minb, qst = policy.get((bp, deg),
+                                           (TARGET_THREADS, min_blocks(bp, deg), 0))
+            n, m, epb, nt, ph, lays, ebufs, qs, ord_ = plan(bp, deg, target, bool(qst))
             out.append(f"template <> struct Cfg<{bp}, {deg}> {{")
             out.append(f"  static constexpr int EPB = {epb}, NT = {nt}, MINB = {minb};")
+            out.append(f"  static constexpr int QS = {qs};  // TMA q-staging slab stride (0: off)")
+            out.append(f"  static constexpr int ORD = {ord_};  // lane orders (BP1.0: bit0 j-, bit1 i-lines k-fastest)")
             out.append("  static constexpr int EBUF[%d] = {%s};" % (
                 len(ebufs), ", ".join(str(e) for e in ebufs)))
             out.append("  static constexpr Lay L[%d] = {%s};" % (
@@ -153,10 +199,12 @@ def main(path, policy=None, verbose=False):
 
 
 def load_policy(path):
-    """JSON list of [bp, deg, target_threads, min_blocks] (tools/tune_policy.json)."""
+    """JSON list of [bp, deg, target_threads, min_blocks(, qstage)]
+    (tools/tune_policy.json)."""
     import json
     with open(path) as fh:
-        return {(int(b), int(d)): (int(t), int(mb)) for b, d, t, mb in json.load(fh)}
+        return {(int(r[0]), int(r[1])): (int(r[2]), int(r[3]), int(r[4]) if len(r) > 4 else 0)
+                for r in json.load(fh)}
 
 
 if __name__ == "__main__":
