@@ -120,3 +120,91 @@ def rel_inf(a, b):
     if b.size == 0:
         return 0.0
     return float(np.max(np.abs(a - b)) / max(1.0, float(np.max(np.abs(b)))))
+
+
+# ---- assembly on the structured cube mesh (checker for csrc/hx_dss.cu) ------
+# The reference has no assembly, so nothing here is pinned to a
+# reference output: these restate Q / Q^T as plain index arithmetic on
+# build_cube_mesh's element order (mesh.py:44-56: e = (cx*side + cy)*side + cz,
+# r/s/t = x/y/z) and are checked in tests against dense linear algebra.
+
+def cube_global_index(side, degree):
+    """(E, n^3) global node id of every element-local node."""
+    n, N = degree + 1, degree
+    g1 = side * N + 1
+    e = np.arange(side ** 3)
+    cx, cy, cz = e // (side * side), (e // side) % side, e % side
+    k, j, i = np.meshgrid(np.arange(n), np.arange(n), np.arange(n), indexing="ij")
+    gx = cx[:, None] * N + i.ravel()[None, :]
+    gy = cy[:, None] * N + j.ravel()[None, :]
+    gz = cz[:, None] * N + k.ravel()[None, :]
+    return (gx * g1 + gy) * g1 + gz
+
+
+def cube_boundary(side, degree):
+    """(n_global,) bool: node lies on the cube boundary."""
+    g1 = side * degree + 1
+    gx, gy, gz = np.meshgrid(np.arange(g1), np.arange(g1), np.arange(g1), indexing="ij")
+    b = (gx == 0) | (gx == g1 - 1) | (gy == 0) | (gy == g1 - 1) | (gz == 0) | (gz == g1 - 1)
+    return b.ravel()
+
+
+def scatter_add(u, gidx, n_global):
+    """Q^T u: sum element-local values into global nodes."""
+    out = np.zeros(n_global)
+    np.add.at(out, gidx.ravel(), np.asarray(u, dtype=np.float64).ravel())
+    return out
+
+
+def dss(u, side, degree, mask=False):
+    """mask . Q Q^T u, element-local in and out."""
+    gidx = cube_global_index(side, degree)
+    ng = (side * degree + 1) ** 3
+    s = scatter_add(u, gidx, ng)
+    if mask:
+        s[cube_boundary(side, degree)] = 0.0
+    return s[gidx].reshape(np.shape(u))
+
+
+def multiplicity(side, degree):
+    gidx = cube_global_index(side, degree)
+    cnt = np.bincount(gidx.ravel(), minlength=(side * degree + 1) ** 3)
+    return cnt[gidx]
+
+
+_CORNERS = np.array([[a, b, c] for a in (-1.0, 1.0) for b in (-1.0, 1.0) for c in (-1.0, 1.0)])
+
+
+def node_coords(vertices, nodes):
+    """(E, n^3, 3) physical coordinates of every element-local node under the
+    trilinear map (reference mesh.py:93-98, corner order mesh.py:9), batched:
+    node (k, j, i) sits at reference point (nodes[i], nodes[j], nodes[k])."""
+    v = np.asarray(vertices, dtype=np.float64)
+    r = np.asarray(nodes, dtype=np.float64)
+    n = r.size
+    t, s, q = np.meshgrid(r, r, r, indexing="ij")          # (k, j, i) grids
+    pts = np.stack([q.ravel(), s.ravel(), t.ravel()], axis=1)  # (n^3, 3) = (r, s, t)
+    phi = np.prod(1 + pts[:, None, :] * _CORNERS[None, :, :], axis=2) / 8.0  # (n^3, 8)
+    return np.einsum("pc,ecd->epd", phi, v).reshape(v.shape[0], n ** 3, 3)
+
+
+def assembled_cg(apply, b, side, degree, mask, tol=1e-13, maxiter=2000):
+    """CG on mask Q^T A_L Q with continuous element-local representatives (the
+    algorithm of cg.cg_solve_assembled, in numpy).  Returns (x, iterations)."""
+    mult = multiplicity(side, degree)
+    r = dss(b, side, degree, mask)
+    x = np.zeros_like(r)
+    p = r.copy()
+    rr = np.sum(r * r / mult)
+    r0 = np.sqrt(rr)
+    for it in range(maxiter):
+        ap = apply(p)
+        alpha = rr / np.sum(p * ap)
+        x += alpha * p
+        r -= alpha * dss(ap, side, degree, mask)
+        rn = np.sum(r * r / mult)
+        if np.sqrt(rn) < tol * r0:
+            return x, it + 1
+        p = r + rn / rr * p
+        rr = rn
+    return x, maxiter

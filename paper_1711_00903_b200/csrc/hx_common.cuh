@@ -222,6 +222,32 @@ __device__ __forceinline__ void line_coords(int ln, int& first, int& second) {
   }
 }
 
+// (k, a) of i-line `ln` over an (n x m) grid of lines in the lane order ORD
+// picked by tools/gen_layouts.py: 0 a fastest; 2 k fastest; 4 k-paired (k
+// pairs outermost, then a, then the k parity fastest; an odd last slice is
+// enumerated alone) -- paired with k-paired layouts (Lay::sq) this keeps both
+// the i-lines and the (k, i) j-lines of a tensor free of bank conflicts.
+template <int n, int m, int ORD>
+__device__ __forceinline__ void iline_coords(int ln, int& k, int& a) {
+  if constexpr (ORD == 2) {
+    k = ln % n;
+    a = ln / n;
+  } else if constexpr (ORD == 4) {
+    constexpr int FULL = (n / 2) * 2 * m;
+    if (FULL == n * m || ln < FULL) {
+      const int kh = ln / (2 * m), r = ln % (2 * m);
+      k = 2 * kh + (r & 1);
+      a = r >> 1;
+    } else {
+      k = n - 1;
+      a = ln - FULL;
+    }
+  } else {
+    k = ln / m;
+    a = ln % m;
+  }
+}
+
 // Sum of one double per thread over the CTA (result valid in thread 0).
 // `scratch` is shared memory of at least NT/32 doubles that no thread is
 // still reading.

@@ -38,8 +38,10 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT)
   constexpr int EPB = C::EPB, NT = C::NT;
   constexpr Lay LX = C::L[0], LY = C::L[1];
   constexpr int EX = C::EBUF[0], EY = C::EBUF[1];
-  // lane orders of the j-line (S1, S5) and i-line (S2, S4) stages: k fastest
-  constexpr bool JKF = C::ORD & 1, IKF = C::ORD & 2;
+  // lane order of the i-line stages (S2, S4), see iline_coords; the j-line
+  // stages (S1, S5) touch HBM and keep i fastest
+  constexpr int IORD = C::ORD;
+  constexpr bool JKF = false;
   extern __shared__ double smem[];
   double* const X = smem;
   double* const Y = X + EPB * EX;
@@ -66,7 +68,7 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT)
         }
         if (bad && p.flag) atomicOr(p.flag, 1);
         fold_apply<m, n, 1>(p.I, x, y);
-        double* dst = X + el * EX + k * LX.s0 + i;
+        double* dst = X + el * EX + LX.kofs(k) + i;
 #pragma unroll
         for (int t = 0; t < m; ++t) dst[t * LX.s1] = y[t];
       });
@@ -75,13 +77,13 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT)
         const int el = g / (n * m), ln = g % (n * m);
         if (el >= ne) return;
         int k, a;
-        line_coords<n, m, IKF>(ln, k, a);
-        const double* src = X + el * EX + k * LX.s0 + a * LX.s1;
+        iline_coords<n, m, IORD>(ln, k, a);
+        const double* src = X + el * EX + LX.kofs(k) + a * LX.s1;
         double x[n], y[m];
 #pragma unroll
         for (int t = 0; t < n; ++t) x[t] = src[t];
         fold_apply<m, n, 1>(p.I, x, y);
-        double* dst = Y + el * EY + k * LY.s0 + a * LY.s1;
+        double* dst = Y + el * EY + LY.kofs(k) + a * LY.s1;
 #pragma unroll
         for (int t = 0; t < m; ++t) dst[t] = y[t];
       });
@@ -93,7 +95,7 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT)
         const double* line = Y + el * EY + a * LY.s1 + c;
         double x[n], y[m];
 #pragma unroll
-        for (int t = 0; t < n; ++t) x[t] = line[t * LY.s0];
+        for (int t = 0; t < n; ++t) x[t] = line[LY.kofs(t)];
         fold_apply<m, n, 1>(p.I, x, y);
         double* dst = p.dst + (e0 + el) * DST + ln;
 #pragma unroll
@@ -116,20 +118,20 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT)
         fold_apply<n, m, 1>(p.It, x, y);
         double* line = Y + el * EY + a * LY.s1 + c;
 #pragma unroll
-        for (int t = 0; t < n; ++t) line[t * LY.s0] = y[t];
+        for (int t = 0; t < n; ++t) line[LY.kofs(t)] = y[t];
       });
       __syncthreads();
       for_lines<EPB * n * m, NT>(tid, [&](int g) {
         const int el = g / (n * m), ln = g % (n * m);
         if (el >= ne) return;
         int k, a;
-        line_coords<n, m, IKF>(ln, k, a);
-        const double* src = Y + el * EY + k * LY.s0 + a * LY.s1;
+        iline_coords<n, m, IORD>(ln, k, a);
+        const double* src = Y + el * EY + LY.kofs(k) + a * LY.s1;
         double x[m], y[n];
 #pragma unroll
         for (int t = 0; t < m; ++t) x[t] = src[t];
         fold_apply<n, m, 1>(p.It, x, y);
-        double* dst = X + el * EX + k * LX.s0 + a * LX.s1;
+        double* dst = X + el * EX + LX.kofs(k) + a * LX.s1;
 #pragma unroll
         for (int t = 0; t < n; ++t) dst[t] = y[t];
       });
@@ -139,7 +141,7 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT)
         if (el >= ne) return;
         int k, i;
         line_coords<n, n, JKF>(ln, k, i);
-        const double* src = X + el * EX + k * LX.s0 + i;
+        const double* src = X + el * EX + LX.kofs(k) + i;
         double x[m], y[n];
 #pragma unroll
         for (int t = 0; t < m; ++t) x[t] = src[t * LX.s1];

@@ -1,0 +1,122 @@
+"""GPU: gather-scatter (hx_dss) and the assembled CG solve
+(cg_solve_assembled) against the oracle's Q Q^T, dense linear algebra and a
+manufactured Poisson solution."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import paper_1711_00903_b200 as hx  # noqa: E402
+from oracle import hexbench_oracle as orc  # noqa: E402
+from paper_1711_00903_b200 import _native  # noqa: E402
+from paper_1711_00903_b200.cg import CGWorkspace, cg_solve_assembled, gather_scatter  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+@pytest.mark.parametrize("side,deg", [(1, 3), (2, 1), (3, 2), (3, 4), (2, 7), (4, 3)])
+@pytest.mark.parametrize("mask", [False, True])
+def test_dss_matches_oracle_and_is_continuous(side, deg, mask):
+    n3 = (deg + 1) ** 3
+    u = np.random.default_rng(side * 10 + deg).standard_normal((side ** 3, n3))
+    got = gather_scatter(torch.from_numpy(u).cuda(), side, deg, mask).cpu().numpy()
+    ref = orc.dss(u, side, deg, mask)
+    assert orc.rel_l2(got, ref) <= 1e-15
+    # every copy of a global node holds the bit-identical sum
+    gidx = orc.cube_global_index(side, deg).ravel()
+    first = np.full(gidx.max() + 1, np.nan)
+    first[gidx[::-1]] = got.ravel()[::-1]
+    np.testing.assert_array_equal(first[gidx], got.ravel())
+
+
+def test_dot_dss_is_global_inner_product():
+    side, deg = 3, 3
+    n3 = (deg + 1) ** 3
+    rng = np.random.default_rng(1)
+    # continuous representatives of two global vectors
+    gidx = orc.cube_global_index(side, deg)
+    ug, vg = rng.standard_normal((2, gidx.max() + 1))
+    u, v = ug[gidx], vg[gidx]
+    dev = [torch.from_numpy(a).cuda() for a in (u, v)]
+    part = torch.empty(_native.lib().hx_energy_partials(), dtype=torch.float64, device="cuda")
+    res = torch.zeros(1, dtype=torch.float64, device="cuda")
+    _native.check(_native.lib().hx_dot_dss(_native.ptr(dev[0]), _native.ptr(dev[1]), side, deg,
+                                           _native.ptr(part), part.numel(), _native.ptr(res),
+                                           None))
+    assert abs(float(res) - float(ug @ vg)) <= 1e-12 * abs(float(ug @ vg))
+    assert u.shape == (side ** 3, n3)
+
+
+def _assembled_case(bp, side, deg, lam):
+    mesh = hx.build_cube_mesh(side, 2.0)
+    op = hx.make_operator(bp, deg, mesh, lam=lam)
+    b = np.random.default_rng(3).standard_normal((mesh.n_el, op.n_p))
+    return mesh, op, b
+
+
+@pytest.mark.parametrize("bp,lam,mask", [(hx.BP35, 0.0, True), (hx.BP3, 0.3, True),
+                                         (hx.BP1, 0.0, False), (hx.BP35, 1.0, False)])
+def test_assembled_cg_matches_oracle_cg(bp, lam, mask):
+    side, deg = 3, 3
+    mesh, op, b = _assembled_case(bp, side, deg, lam)
+    res = cg_solve_assembled(op, side, torch.from_numpy(b).cuda(), tol=1e-12,
+                             mask_boundary=mask)
+    assert res.converged
+    interp = None if op.interp is None else op.interp.entries
+    diff = None if op.diff is None else op.diff.entries
+    ref, _ = orc.assembled_cg(lambda p: orc.apply(bp, deg, lam, interp, diff, op.factors.data, p),
+                       b, side, deg, mask, tol=1e-12)
+    assert orc.rel_l2(res.x.cpu().numpy(), ref) <= 1e-9
+
+
+def test_assembled_cg_matches_dense_solve():
+    """BP3.5 Poisson, Dirichlet: x_G = A_G^{-1} b_G with A_G assembled densely
+    from the oracle element operator (column g = Q^T A_L Q e_g)."""
+    side, deg = 2, 3
+    mesh, op, b = _assembled_case(hx.BP35, side, deg, 0.0)
+    gidx = orc.cube_global_index(side, deg)
+    ng = gidx.max() + 1
+    diff = op.diff.entries
+    fac = op.factors.data
+    cols = np.zeros((ng, ng))
+    for g in range(ng):
+        ul = (gidx == g).astype(float)
+        cols[:, g] = orc.scatter_add(orc.apply(hx.BP35, deg, 0.0, None, diff, fac, ul), gidx, ng)
+    inner = ~orc.cube_boundary(side, deg)
+    bg = orc.scatter_add(b, gidx, ng)
+    xg = np.zeros(ng)
+    xg[inner] = np.linalg.solve(cols[np.ix_(inner, inner)], bg[inner])
+    res = cg_solve_assembled(op, side, torch.from_numpy(b).cuda(), tol=1e-13)
+    assert orc.rel_l2(res.x.cpu().numpy(), xg[gidx]) <= 1e-10
+
+
+def test_poisson_manufactured_solution_spectral_accuracy():
+    """-lap u = f on [0,2]^3, u = prod sin(pi x / 2): BP3.5 stiffness, BP1.0
+    load vector, assembled CG on the device -> max nodal error ~2e-10 at
+    side 3, N = 7 (the oracle solve gives the same)."""
+    side, deg = 3, 7
+    mesh = hx.build_cube_mesh(side, 2.0)
+    x = orc.node_coords(mesh.vertices, hx.gll_rule(deg + 1).nodes)
+    u_ex = np.prod(np.sin(np.pi * x / 2), axis=-1)
+    f = 3 * (np.pi / 2) ** 2 * u_ex
+    mass = hx.make_operator(hx.BP1, deg, mesh)
+    b = hx.apply_operator(mass, hx.FieldVector(mesh.n_el, mass.n_p, torch.from_numpy(f).cuda()))
+    stiff = hx.make_operator(hx.BP35, deg, mesh, lam=0.0)
+    res = cg_solve_assembled(stiff, side, b.data, tol=1e-13, work=CGWorkspace(b.data))
+    assert res.converged and res.iterations < 300
+    assert np.abs(res.x.cpu().numpy() - u_ex).max() < 1e-8
+
+
+def test_dss_argument_errors():
+    u = torch.zeros(8 * 27, dtype=torch.float64, device="cuda")
+    with pytest.raises(ValueError):
+        gather_scatter(u, 3, 2)            # wrong size for the mesh
+    with pytest.raises(ValueError):
+        gather_scatter(u, 2, 2, out=u)     # in-place is rejected

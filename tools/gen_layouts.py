@@ -29,31 +29,48 @@ TARGET_THREADS = 256
 
 def lines(d, pat):
     d0, d1, d2 = d
-    return {0: (d1 * d2, d0), 1: (d0 * d2, d1), 2: (d0 * d1, d2)}[pat % 3]
+    return {0: (d1 * d2, d0), 1: (d0 * d2, d1), 2: (d0 * d1, d2), 5: (d0 * d1, d2),
+            6: (d0 * d1, d2)}[pat]
 
 
-def addr(d, s0, s1, pat, l, t):
+def kofs(lay, k):
+    """Offset of slice k: plain (k * s0), or k-paired when sq > 0: slices 2h
+    and 2h+1 sit sq apart inside a pair block of stride s0."""
+    s0, _, sq = lay
+    return k * s0 if sq == 0 else (k // 2) * s0 + (k % 2) * sq
+
+
+def pair_coords(l, d0, d1):
+    """Pattern 6 lane order over (k, a): k pairs outermost, then a, then the
+    k parity fastest; an odd trailing slice is enumerated alone."""
+    g = 2 * d1
+    full = (d0 // 2) * g
+    if l < full:
+        kh, r = divmod(l, g)
+        a, kl = divmod(r, 2)
+        return 2 * kh + kl, a
+    return d0 - 1, l - full
+
+
+def addr(d, lay, pat, l, t):
     d0, d1, d2 = d
+    s1 = lay[1]
     if pat == 0:
         j, i = divmod(l, d2)
-        return t * s0 + j * s1 + i
+        return kofs(lay, t) + j * s1 + i
     if pat == 1:
         k, i = divmod(l, d2)
-        return k * s0 + t * s1 + i
+        return kofs(lay, k) + t * s1 + i
     if pat == 2:
         k, j = divmod(l, d1)
-        return k * s0 + j * s1 + t
-    if pat == 3:
-        i, j = divmod(l, d1)
-        return t * s0 + j * s1 + i
-    if pat == 4:
-        i, k = divmod(l, d0)
-        return k * s0 + t * s1 + i
-    j, k = divmod(l, d0)
-    return k * s0 + j * s1 + t
+    elif pat == 5:
+        j, k = divmod(l, d0)
+    else:
+        k, j = pair_coords(l, d0, d1)
+    return kofs(lay, k) + j * s1 + t
 
 
-def cost(d, s0, s1, pats, epb, ebuf):
+def cost(d, lay, pats, epb, ebuf):
     total = 0
     for pat in pats:
         nl, ln = lines(d, pat)
@@ -64,7 +81,7 @@ def cost(d, s0, s1, pats, epb, ebuf):
                     words = set()
                     for g in range(w0 + h, min(w0 + h + 16, tot_lines)):
                         e, l = divmod(g, nl)
-                        words.add(e * ebuf + addr(d, s0, s1, pat, l, t))
+                        words.add(e * ebuf + addr(d, lay, pat, l, t))
                     if not words:
                         continue
                     cnt = [0] * 16
@@ -74,16 +91,27 @@ def cost(d, s0, s1, pats, epb, ebuf):
     return total
 
 
-def best_layout(d, pats):
+def extent(d, lay):
+    """Doubles spanned by one element's tensor under `lay`."""
+    d0, d1, d2 = d
+    return kofs(lay, d0 - 1) + (d1 - 1) * lay[1] + d2
+
+
+def best_layout(d, pats, paired=False):
     d0, d1, d2 = d
     best = None
     for s1 in range(d2, d2 + 4):
-        for s0 in range(d1 * s1, d1 * s1 + 16):
-            c = cost(d, s0, s1, pats, 1, 0)
-            key = (c, d0 * s0)
+        if not paired:
+            cands = ((s0, s1, 0) for s0 in range(d1 * s1, d1 * s1 + 16))
+        else:
+            cands = ((s0, s1, sq) for sq in range(d1 * s1, d1 * s1 + 16)
+                     for s0 in range(sq + d1 * s1, sq + d1 * s1 + 16))
+        for lay in cands:
+            c = cost(d, lay, pats, 1, 0)
+            key = (c, extent(d, lay))
             if best is None or key < best[0]:
-                best = (key, s0, s1)
-    return best[1], best[2]
+                best = (key, lay)
+    return best[1]
 
 
 def phases(bp, n, m, ord_=0):
@@ -92,16 +120,18 @@ def phases(bp, n, m, ord_=0):
         return [(0, (n, n, n), (0, 1, 2)), (1, (n, n, n), (0, 2)),
                 (2, (n, n, n), (0, 1))]
     if bp == BP1:
-        # ord bit 0: j-lines k-fastest (4 instead of 1); bit 1: i-lines (5 for 2)
-        pj = 4 if ord_ & 1 else 1
-        pi = 5 if ord_ & 2 else 2
-        return [(0, (n, m, n), (pj, pi)), (1, (n, m, m), (0, pi))]
+        # ORD: lane order of the i-line stages (S2, S4): 0 a fastest (pattern
+        # 2), 2 k fastest (5), 4 k-paired (6, with k-paired layouts).  The
+        # j-line and k-line stages also touch HBM and keep their coalesced
+        # orders (k fastest there doubles the L1 tag requests: ncu r09).
+        pi = {0: 2, 2: 5, 4: 6}[ord_]
+        return [(0, (n, m, n), (1, pi)), (1, (n, m, m), (0, pi))]
     return [(0, (n, m, n), (1, 2)), (0, (m, m, m), (0, 2)),
             (1, (n, m, m), (0, 2)), (1, (m, m, m), (0, 1)),
             (2, (m, m, m), (0, 1, 2)), (2, (n, m, m), (0, 2))]
 
 
-def q_stage_stride(n, ord_=0):
+def q_stage_stride(n):
     """Slab stride (doubles) of BP1.0's TMA-staged q tile: every k-slab
     (n*n doubles, contiguous in HBM) is one bulk copy, so rows stay dense
     (s1 = n) and only the slab stride is free; it must keep 16-byte alignment
@@ -112,7 +142,7 @@ def q_stage_stride(n, ord_=0):
     d = (n, n, n)
     best = None
     for s0 in range(n * n, n * n + 16, 2):
-        c = cost(d, s0, n, (4 if ord_ & 1 else 1,), 1, 0)
+        c = cost(d, (s0, n, 0), (1,), 1, 0)
         if best is None or c < best[0]:
             best = (c, s0)
     return best[1]
@@ -127,20 +157,20 @@ def plan(bp, deg, target=TARGET_THREADS, qstage=False):
         # BP1.0 only: a CTA smaller than one element's line count walks over
         # the lines (for_lines); one element per tile
         nt = max(32, -(-target // 32) * 32)
-    ords = (0, 1, 2, 3) if bp == BP1 else (0,)
+    ords = (0, 2, 4) if bp == BP1 else (0,)
     best = None
     for o in ords:  # BP1.0: lane orders chosen jointly with the strides
         ph_o = phases(bp, n, m, o)
-        lays_o = [best_layout(d, pats) for _, d, pats in ph_o]
-        c = sum(cost(d, s0, s1, pats, 1, 0) for (_, d, pats), (s0, s1) in zip(ph_o, lays_o))
+        lays_o = [best_layout(d, pats, paired=(o == 4)) for _, d, pats in ph_o]
+        c = sum(cost(d, lay, pats, 1, 0) for (_, d, pats), lay in zip(ph_o, lays_o))
         if best is None or c < best[0]:
             best = (c, o, ph_o, lays_o)
     _, ord_, ph, lays = best
     nbuf = 1 + max(b for b, _, _ in ph)
     base = [0] * nbuf
-    for (b, d, _), (s0, _) in zip(ph, lays):
-        base[b] = max(base[b], d[0] * s0)
-    qs = q_stage_stride(n, ord_) if (bp == BP1 and qstage) else 0
+    for (b, d, _), lay in zip(ph, lays):
+        base[b] = max(base[b], max(extent(d, lay), d[0] * lay[0] if lay[2] == 0 else 0))
+    qs = q_stage_stride(n) if (bp == BP1 and qstage) else 0
     # keep the tile inside the 227 KB shared-memory limit
     while epb > 1 and epb * (sum(base) + 16 * nbuf + n * qs) * 8 > 227 * 1024:
         epb -= 1
@@ -149,8 +179,8 @@ def plan(bp, deg, target=TARGET_THREADS, qstage=False):
     for b in range(nbuf):
         best = None
         for eb in range(base[b], base[b] + 16):
-            c = sum(cost(d, s0, s1, pats, epb, eb)
-                    for (bb, d, pats), (s0, s1) in zip(ph, lays) if bb == b)
+            c = sum(cost(d, lay, pats, epb, eb)
+                    for (bb, d, pats), lay in zip(ph, lays) if bb == b)
             if best is None or c < best[0]:
                 best = (c, eb)
         ebufs.append(best[1])
@@ -175,7 +205,14 @@ def main(path, policy=None, verbose=False):
            "// Shared-memory strides per (kernel, degree): see that script for the",
            "// bank model.  Phase order follows the kernels' stage order.",
            "#pragma once", "", "namespace hx {", "",
-           "struct Lay { int s0, s1; };", "",
+           "// element (k, j, i) of a staged tensor lives at kofs(k) + j*s1 + i with",
+           "// kofs(k) = k*s0, or (k/2)*s0 + (k%2)*sq for a k-paired layout (sq > 0)",
+           "struct Lay {",
+           "  int s0, s1, sq;",
+           "  __host__ __device__ constexpr int kofs(int k) const {",
+           "    return sq == 0 ? k * s0 : (k >> 1) * s0 + (k & 1) * sq;",
+           "  }",
+           "};", "",
            "template <int BP, int N> struct Cfg;", ""]
     for bp in (BP1, BP35, BP3):
         for deg in range(1, 16):
@@ -185,11 +222,11 @@ def main(path, policy=None, verbose=False):
             out.append(f"template <> struct Cfg<{bp}, {deg}> {{")
             out.append(f"  static constexpr int EPB = {epb}, NT = {nt}, MINB = {minb};")
             out.append(f"  static constexpr int QS = {qs};  // TMA q-staging slab stride (0: off)")
-            out.append(f"  static constexpr int ORD = {ord_};  // lane orders (BP1.0: bit0 j-, bit1 i-lines k-fastest)")
+            out.append(f"  static constexpr int ORD = {ord_};  // BP1.0 i-line lane order: 0, 2 k-fast, 4 k-paired")
             out.append("  static constexpr int EBUF[%d] = {%s};" % (
                 len(ebufs), ", ".join(str(e) for e in ebufs)))
             out.append("  static constexpr Lay L[%d] = {%s};" % (
-                len(lays), ", ".join("{%d, %d}" % l for l in lays)))
+                len(lays), ", ".join("{%d, %d, %d}" % l for l in lays)))
             out.append("};")
             if verbose:
                 sys.stderr.write(f"bp={bp} N={deg} epb={epb} nt={nt} ebuf={ebufs} lays={lays}\n")
