@@ -385,6 +385,42 @@ def cg_report(op, mesh, iters=20, warmup=3):
             "kernels_per_iteration": 5}
 
 
+def cg_assembled_report(side=32, iters=20, warmup=3):
+    """Assembled CG (cg.cg_solve_assembled: Poisson, BP3.5 N=7 on the
+    unperturbed side^3 cube mesh, Dirichlet mask): fused matvec + <p,Ap>, the
+    update with the gather-scatter of A p fused in, direction.  Same 9 vector
+    passes per iteration as the element-local CG; the DSS gathers re-read
+    shared-node neighbours (L2 hits)."""
+    import torch
+    import paper_1711_00903_b200 as hx
+    from paper_1711_00903_b200.cg import CGWorkspace, cg_iterations_assembled
+
+    mesh = hx.build_cube_mesh(side, 2.0)
+    op = hx.make_operator(hx.BP35, DEGREE, mesh, lam=0.0)
+    b = torch.randn(op.n_el, op.n_p, dtype=torch.float64, device="cuda")
+    w = CGWorkspace(b)
+
+    def timed(k):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        cg_iterations_assembled(op, side, b, k, w)
+        e.record()
+        e.synchronize()
+        return s.elapsed_time(e)
+
+    timed(warmup)
+    ms = (timed(iters) - timed(0)) / iters
+    per_el = hx.traffic(op.bp, op.degree).bytes_per_element + 9 * 8 * op.n_p
+    unique = (side * DEGREE + 1) ** 3
+    return {"bp": op.bp, "degree": op.degree, "n_el": op.n_el, "side": side,
+            "global_dofs": unique, "ms_per_iteration": ms,
+            "gdof_iterations_per_s": op.n_el * op.n_p / (ms * 1e-3) / 1e9,
+            "global_gdof_iterations_per_s": unique / (ms * 1e-3) / 1e9,
+            "hbm_bytes_per_iteration": per_el * op.n_el,
+            "achieved_gb_per_s": per_el * op.n_el / (ms * 1e-3) / 1e9,
+            "kernels_per_iteration": 5}
+
+
 def run_ours(args):
     import torch
     import paper_1711_00903_b200 as hx
@@ -434,6 +470,7 @@ def run_ours(args):
         e2e["pcie"] = pcie
         e2e["frac_of_pcie_bound"] = pcie["bidirectional_ms"] / e2e_ms
     cg = cg_report(op, mesh) if (rank == 0 and not args.quick) else None
+    cg_asm = cg_assembled_report() if (rank == 0 and not args.quick) else None
     calib = None
     if rank == 0 and not args.quick:
         import ctypes
@@ -489,6 +526,7 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "per_bp": per_bp,
             "cg": cg,
+            "cg_assembled": cg_asm,
             "calibration": calib,
             "gflop_per_s": hx.flop_model(bp, "fused", DEGREE) * dofs_all / (DEGREE + 1) ** 3
                            / (ms_per_step * 1e-3) / 1e9,

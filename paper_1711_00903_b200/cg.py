@@ -230,3 +230,32 @@ def cg_solve_assembled(op, side, b, tol=1e-10, maxiter=1000, check_every=10,
     if int(flag.item()) & _native.HX_FLAG_NONFINITE:
         raise ValueError("non-finite values during the CG solve")
     return CGResult(x, it, converged, norms)
+
+
+def cg_iterations_assembled(op, side, b, iterations, work, mask_boundary=True, stream=None):
+    """``iterations`` assembled-CG steps from x = 0 with no convergence checks
+    or host synchronisation (the harness times this)."""
+    import torch
+
+    L = _native.lib()
+    ptr = _native.ptr
+    deg = op.degree
+    n = b.numel()
+    stream = _stream(op.device) if stream is None else stream
+    mask = int(bool(mask_boundary))
+    x = torch.zeros_like(b)
+    w = work
+    gather_scatter(b, side, deg, mask_boundary, out=w.r, stream=stream)
+    w.p.copy_(w.r)
+    cur = 0
+    L.hx_dot_dss(ptr(w.r), ptr(w.r), side, deg, ptr(w.partials), w.npart, ptr(w.rr[cur]), stream)
+    for _ in range(iterations):
+        nxt = 1 - cur
+        L.hx_apply_energy(op.plan.handle, ptr(w.p), ptr(op.device_factors), ptr(w.ap),
+                          op.n_el, ptr(w.partials), w.npart, ptr(w.pap), None, stream)
+        L.hx_cg_update_dss(ptr(x), ptr(w.p), ptr(w.r), ptr(w.ap), side, deg, mask,
+                           ptr(w.rr[cur]), ptr(w.pap), ptr(w.partials), w.npart,
+                           ptr(w.rr[nxt]), stream)
+        L.hx_cg_direction(ptr(w.p), ptr(w.r), n, ptr(w.rr[nxt]), ptr(w.rr[cur]), stream)
+        cur = nxt
+    return x

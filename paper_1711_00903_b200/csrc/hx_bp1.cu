@@ -135,12 +135,9 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT, HX_MINB_BP1_OF(N))
       line_coords<n, n, JKF>(ln, k, i);
       const double* src = QST ? QT + (el * n + k) * QS + i : p.q + (e0 + el) * n3 + k * n2 + i;
       double x[n], y[m];
-      bool bad = false;
 #pragma unroll
-      for (int t = 0; t < n; ++t) {
-        x[t] = src[t * n];
-        bad |= nonfinite(x[t]);
-      }
+      for (int t = 0; t < n; ++t) x[t] = src[t * n];
+      const bool bad = any_nonfinite(x);
       if (bad && p.flag) atomicOr(p.flag, 1);
       fold_apply<m, n, 1>(p.I, x, y);
       double* dst = X + el * EX + LX.kofs(k) + i;

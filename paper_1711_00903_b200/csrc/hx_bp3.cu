@@ -107,12 +107,9 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT, HX_MINB_BP3_OF(N))
       const int k = ln_a / n, i = ln_a % n;
       const double* src = p.q + (e0 + el_a) * n3 + k * n2 + i;
       double x[n], y[m];
-      bool bad = false;
 #pragma unroll
-      for (int t = 0; t < n; ++t) {
-        x[t] = src[t * n];
-        bad |= nonfinite(x[t]);
-      }
+      for (int t = 0; t < n; ++t) x[t] = src[t * n];
+      const bool bad = any_nonfinite(x);
       if (bad && p.flag) atomicOr(p.flag, 1);
       fold_apply<m, n, 1>(p.I, x, y);
       double* dst = Aa + k * LX.s0 + i;

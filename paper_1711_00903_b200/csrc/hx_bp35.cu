@@ -96,12 +96,9 @@ __global__ void __launch_bounds__(Cfg<kBP35, N>::NT, HX_MINB_BP35_OF(N))
     if (act) {
       const int j = ln / n, i = ln % n;
       const double* src = p.q + e * n3 + j * n + i;
-      bool bad = false;
 #pragma unroll
-      for (int k = 0; k < n; ++k) {
-        qv[k] = src[k * n2];
-        bad |= nonfinite(qv[k]);
-      }
+      for (int k = 0; k < n; ++k) qv[k] = src[k * n2];
+      const bool bad = any_nonfinite(qv);
       if (bad && p.flag) atomicOr(p.flag, 1);
       fold_apply<n, n, -1>(p.D, qv, qt);
       double* a = Ae + j * LA.s1 + i;

@@ -174,6 +174,18 @@ __device__ __forceinline__ bool nonfinite(double v) {
   return (__double_as_longlong(v) & 0x7ff0000000000000ll) == 0x7ff0000000000000ll;
 }
 
+// Any inf / nan in a loaded line, on the integer pipe: (~hi & EXP) is 0 iff
+// the exponent bits of the high word are all ones; one LOP3 + IMNMX per value
+// instead of an FP64-pipe DSETP (the FP64 pipe is the busier one).
+template <int L>
+__device__ __forceinline__ bool any_nonfinite(const double (&x)[L]) {
+  unsigned acc = 0x7ff00000u;
+#pragma unroll
+  for (int t = 0; t < L; ++t)
+    acc = min(acc, ~static_cast<unsigned>(__double2hiint(x[t])) & 0x7ff00000u);
+  return acc == 0u;
+}
+
 // Load the j-line (k, i) = divmod(line, n) of one element's (n, n, n) field:
 // q[k][0..n-1][i] -- 8n-byte runs across the lanes of a warp.
 template <int n>

@@ -60,12 +60,9 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT)
         line_coords<n, n, JKF>(ln, k, i);
         const double* src = p.src + (e0 + el) * SRC + k * n2 + i;
         double x[n], y[m];
-        bool bad = false;
 #pragma unroll
-        for (int t = 0; t < n; ++t) {
-          x[t] = src[t * n];
-          bad |= nonfinite(x[t]);
-        }
+        for (int t = 0; t < n; ++t) x[t] = src[t * n];
+        const bool bad = any_nonfinite(x);
         if (bad && p.flag) atomicOr(p.flag, 1);
         fold_apply<m, n, 1>(p.I, x, y);
         double* dst = X + el * EX + LX.kofs(k) + i;
@@ -108,12 +105,9 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT)
         const int a = ln / m, c = ln % m;
         const double* src = p.src + (e0 + el) * SRC + ln;
         double x[m], y[n];
-        bool bad = false;
 #pragma unroll
-        for (int t = 0; t < m; ++t) {
-          x[t] = src[t * m2];
-          bad |= nonfinite(x[t]);
-        }
+        for (int t = 0; t < m; ++t) x[t] = src[t * m2];
+        const bool bad = any_nonfinite(x);
         if (bad && p.flag) atomicOr(p.flag, 1);
         fold_apply<n, m, 1>(p.It, x, y);
         double* line = Y + el * EY + a * LY.s1 + c;
