@@ -20,6 +20,12 @@
 //   S7 k-lines (a,c)  m^2 : acc += A + B;  I_t^T acc -> C as Z[k][a][c] L[5]
 //   S8 i-lines (k,a)  n*m : Z -> I_r^T -> A as W[k][a][i]              L[0]
 //   S9 j-lines (k,i)  n^2 : W -> I_s^T -> out (HBM)
+//
+// Cfg::ORD = 4 (tools/gen_layouts.py): the shared-memory-only i-line stages
+// over the (n, m, .) tensors (S2, S8) enumerate their lines k-paired
+// (iline_coords) and those tensors use k-paired layouts (Lay::kofs), which
+// removes the bank conflicts an affine layout cannot avoid for both the
+// i-lines and the (k, i) j-lines of X / W.
 #include "hx_common.cuh"
 #include "hx_plan.h"
 
@@ -112,7 +118,7 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT, HX_MINB_BP3_OF(N))
       const bool bad = any_nonfinite(x);
       if (bad && p.flag) atomicOr(p.flag, 1);
       fold_apply<m, n, 1>(p.I, x, y);
-      double* dst = Aa + k * LX.s0 + i;
+      double* dst = Aa + LX.kofs(k) + i;
 #pragma unroll
       for (int t = 0; t < m; ++t) dst[t * LX.s1] = y[t];
     }
@@ -120,13 +126,14 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT, HX_MINB_BP3_OF(N))
     // ---- S2: i-lines (k, a): interpolate along r
     if (HX_PF_BP3 == 2 && tid == 0) prefetch_l2(p.fac + e0 * fs, ne * fs * sizeof(double));
     if (el_b < ne) {
-      const int k = ln_b / m, a = ln_b % m;
-      const double* src = Ab + k * LX.s0 + a * LX.s1;
+      int k, a;
+      iline_coords<n, m, C::ORD>(ln_b, k, a);
+      const double* src = Ab + LX.kofs(k) + a * LX.s1;
       double x[n], y[m];
 #pragma unroll
       for (int t = 0; t < n; ++t) x[t] = src[t];
       fold_apply<m, n, 1>(p.I, x, y);
-      double* dst = Bb + k * LY.s0 + a * LY.s1;
+      double* dst = Bb + LY.kofs(k) + a * LY.s1;
 #pragma unroll
       for (int t = 0; t < m; ++t) dst[t] = y[t];
     }
@@ -142,7 +149,7 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT, HX_MINB_BP3_OF(N))
       const double* src = Bc + ca * LY.s1 + cc;
       double x[n], tv[m];
 #pragma unroll
-      for (int t = 0; t < n; ++t) x[t] = src[t * LY.s0];
+      for (int t = 0; t < n; ++t) x[t] = src[LY.kofs(t)];
       fold_apply<m, n, 1>(p.I, x, tv);
       if constexpr (!kReread) {
 #pragma unroll
@@ -151,7 +158,7 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT, HX_MINB_BP3_OF(N))
       }
       double* dst = Cc + ca * LT.s1 + cc;
 #pragma unroll
-      for (int t = 0; t < m; ++t) dst[t * LT.s0] = tv[t];
+      for (int t = 0; t < m; ++t) dst[LT.kofs(t)] = tv[t];
     }
     __syncthreads();
     // ---- S4: r- and s-derivatives of T
@@ -159,18 +166,18 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT, HX_MINB_BP3_OF(N))
     if (act_c) {
       const int kk = ln_c / m, r = ln_c % m;
       double x[m], y[m];
-      const double* src = Cc + kk * LT.s0 + r * LT.s1;  // i-line (kk, a=r)
+      const double* src = Cc + LT.kofs(kk) + r * LT.s1;  // i-line (kk, a=r)
 #pragma unroll
       for (int t = 0; t < m; ++t) x[t] = src[t];
       fold_apply<m, m, -1>(p.D, x, y);
-      double* dst = Ac + kk * LQR.s0 + r * LQR.s1;
+      double* dst = Ac + LQR.kofs(kk) + r * LQR.s1;
 #pragma unroll
       for (int t = 0; t < m; ++t) dst[t] = y[t];
-      src = Cc + kk * LT.s0 + r;  // j-line (kk, c=r)
+      src = Cc + LT.kofs(kk) + r;  // j-line (kk, c=r)
 #pragma unroll
       for (int t = 0; t < m; ++t) x[t] = src[t * LT.s1];
       fold_apply<m, m, -1>(p.D, x, y);
-      dst = Bc + kk * LQS.s0 + r;
+      dst = Bc + LQS.kofs(kk) + r;
 #pragma unroll
       for (int t = 0; t < m; ++t) dst[t * LQS.s1] = y[t];
     }
@@ -185,7 +192,7 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT, HX_MINB_BP3_OF(N))
         // re-read this thread's own T k-line (still intact in C)
         const double* tl = Cc + ca * LT.s1 + cc;
 #pragma unroll
-        for (int t = 0; t < m; ++t) tv[t] = tl[t * LT.s0];
+        for (int t = 0; t < m; ++t) tv[t] = tl[LT.kofs(t)];
         fold_apply<m, m, -1>(p.D, tv, tt);
       } else {
 #pragma unroll
@@ -200,11 +207,11 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT, HX_MINB_BP3_OF(N))
         const double grr = gk[0], grs = gk[ss], grt = gk[2 * ss];
         const double gss = gk[3 * ss], gst = gk[4 * ss], gtt = gk[5 * ss];
         const double gwj = gk[6 * ss];
-        const double qr = qrl[t * LQR.s0], qs = qsl[t * LQS.s0], qt = tt[t];
+        const double qr = qrl[LQR.kofs(t)], qs = qsl[LQS.kofs(t)], qt = tt[t];
         const double rqr = grr * qr + grs * qs + grt * qt;
         const double rqs = grs * qr + gss * qs + gst * qt;
-        qrl[t * LQR.s0] = rqr;
-        qsl[t * LQS.s0] = rqs;
+        qrl[LQR.kofs(t)] = rqr;
+        qsl[LQS.kofs(t)] = rqs;
         rqt[t] = grt * qr + gst * qs + gtt * qt;
         const double lt = p.lam * gwj * tv[t];
         // <q, A q> = sum over GL points of grad t . G grad t + lam GwJ t^2
@@ -227,13 +234,13 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT, HX_MINB_BP3_OF(N))
     if (act_c) {
       const int kk = ln_c / m, r = ln_c % m;
       double x[m], y[m];
-      double* l = Ac + kk * LQR.s0 + r * LQR.s1;
+      double* l = Ac + LQR.kofs(kk) + r * LQR.s1;
 #pragma unroll
       for (int t = 0; t < m; ++t) x[t] = l[t];
       fold_apply<m, m, -1>(p.Dt, x, y);
 #pragma unroll
       for (int t = 0; t < m; ++t) l[t] = y[t];
-      l = Bc + kk * LQS.s0 + r;
+      l = Bc + LQS.kofs(kk) + r;
 #pragma unroll
       for (int t = 0; t < m; ++t) x[t] = l[t * LQS.s1];
       fold_apply<m, m, -1>(p.Dt, x, y);
@@ -246,23 +253,24 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT, HX_MINB_BP3_OF(N))
       const double* qrl = Ac + ca * LQR.s1 + cc;
       const double* qsl = Bc + ca * LQS.s1 + cc;
 #pragma unroll
-      for (int t = 0; t < m; ++t) acc[t] += qrl[t * LQR.s0] + qsl[t * LQS.s0];
+      for (int t = 0; t < m; ++t) acc[t] += qrl[LQR.kofs(t)] + qsl[LQS.kofs(t)];
       double y[n];
       fold_apply<n, m, 1>(p.It, acc, y);
       double* dst = Cc + ca * LZ.s1 + cc;
 #pragma unroll
-      for (int t = 0; t < n; ++t) dst[t * LZ.s0] = y[t];
+      for (int t = 0; t < n; ++t) dst[LZ.kofs(t)] = y[t];
     }
     __syncthreads();
     // ---- S8: i-lines (k, a): project along r
     if (el_b < ne) {
-      const int k = ln_b / m, a = ln_b % m;
-      const double* src = Cb + k * LZ.s0 + a * LZ.s1;
+      int k, a;
+      iline_coords<n, m, C::ORD>(ln_b, k, a);
+      const double* src = Cb + LZ.kofs(k) + a * LZ.s1;
       double x[m], y[n];
 #pragma unroll
       for (int t = 0; t < m; ++t) x[t] = src[t];
       fold_apply<n, m, 1>(p.It, x, y);
-      double* dst = Ab + k * LX.s0 + a * LX.s1;
+      double* dst = Ab + LX.kofs(k) + a * LX.s1;
 #pragma unroll
       for (int t = 0; t < n; ++t) dst[t] = y[t];
     }
@@ -270,7 +278,7 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT, HX_MINB_BP3_OF(N))
     // ---- S9: j-lines (k, i): project along s and store
     if (el_a < ne) {
       const int k = ln_a / n, i = ln_a % n;
-      const double* src = Aa + k * LX.s0 + i;
+      const double* src = Aa + LX.kofs(k) + i;
       double x[m], y[n];
 #pragma unroll
       for (int t = 0; t < m; ++t) x[t] = src[t * LX.s1];

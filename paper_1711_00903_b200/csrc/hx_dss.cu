@@ -27,12 +27,6 @@ namespace hx {
 
 constexpr int kDssThreads = 256;
 
-struct DssGeom {
-  int side, n;        // elements per cube side, GLL points per axis (N + 1)
-  int64_t n3, ndof;   // n^3, side^3 n^3
-  int mask;           // zero boundary nodes
-};
-
 // Copies of one local node along one axis: element offsets (in that axis'
 // element coordinate) and local indices, ascending by element.
 struct AxisCopies {
@@ -52,147 +46,164 @@ __device__ __forceinline__ AxisCopies axis_copies(int c, int i, int side, int N)
   return a;
 }
 
+// One element-local node: its element (and that element's cube coordinates,
+// computed once per element by the caller) and its (k, j, i).
 struct NodeRef {
   int64_t e;
-  int k, j, i, cx, cy, cz;
+  int cx, cy, cz, k, j, i;
 };
 
-__device__ __forceinline__ NodeRef decompose(int64_t idx, const DssGeom& g) {
-  NodeRef r;
-  r.e = idx / g.n3;
-  const int loc = int(idx - r.e * g.n3);
-  r.i = loc % g.n;
-  r.j = (loc / g.n) % g.n;
-  r.k = loc / (g.n * g.n);
-  const int64_t s = g.side;
-  r.cz = int(r.e % s);
-  r.cy = int((r.e / s) % s);
-  r.cx = int(r.e / (s * s));
-  return r;
-}
-
-__device__ __forceinline__ bool on_boundary(const NodeRef& r, const DssGeom& g) {
-  const int N = g.n - 1, G = g.side * N;
+template <int N>
+__device__ __forceinline__ bool on_boundary(const NodeRef& r, int side) {
+  const int G = side * N;
   const int gx = r.cx * N + r.i, gy = r.cy * N + r.j, gz = r.cz * N + r.k;
   return gx == 0 || gx == G || gy == 0 || gy == G || gz == 0 || gz == G;
 }
 
 // number of element-local copies of node r
-__device__ __forceinline__ int node_mult(const NodeRef& r, const DssGeom& g) {
-  const int N = g.n - 1;
-  return axis_copies(r.cx, r.i, g.side, N).cnt * axis_copies(r.cy, r.j, g.side, N).cnt *
-         axis_copies(r.cz, r.k, g.side, N).cnt;
+template <int N>
+__device__ __forceinline__ int node_mult(const NodeRef& r, int side) {
+  return axis_copies(r.cx, r.i, side, N).cnt * axis_copies(r.cy, r.j, side, N).cnt *
+         axis_copies(r.cz, r.k, side, N).cnt;
 }
 
 // sum over the copies of node r, in the canonical order
+template <int N>
 __device__ __forceinline__ double gather_sum(const double* __restrict__ u, const NodeRef& r,
-                                             const DssGeom& g) {
-  const int N = g.n - 1;
-  const AxisCopies ax = axis_copies(r.cx, r.i, g.side, N);
-  const AxisCopies ay = axis_copies(r.cy, r.j, g.side, N);
-  const AxisCopies az = axis_copies(r.cz, r.k, g.side, N);
-  const int64_t s = g.side;
+                                             int side) {
+  constexpr int n = N + 1, n3 = n * n * n;
+  const AxisCopies ax = axis_copies(r.cx, r.i, side, N);
+  const AxisCopies ay = axis_copies(r.cy, r.j, side, N);
+  const AxisCopies az = axis_copies(r.cz, r.k, side, N);
+  const int64_t s = side;
   double sum = 0.0;
   for (int a = 0; a < ax.cnt; ++a)
     for (int b = 0; b < ay.cnt; ++b)
       for (int c = 0; c < az.cnt; ++c) {
         const int64_t e = r.e + ax.d[a] * s * s + ay.d[b] * s + az.d[c];
-        sum += u[e * g.n3 + (int64_t(az.l[c]) * g.n + ay.l[b]) * g.n + ax.l[a]];
+        sum += u[e * n3 + (az.l[c] * n + ay.l[b]) * n + ax.l[a]];
       }
   return sum;
 }
 
-__global__ void __launch_bounds__(kDssThreads)
-    dss_kernel(const double* __restrict__ in, double* __restrict__ out, DssGeom g) {
-  for (int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < g.ndof;
-       idx += int64_t(gridDim.x) * blockDim.x) {
-    const NodeRef r = decompose(idx, g);
-    out[idx] = (g.mask && on_boundary(r, g)) ? 0.0 : gather_sum(in, r, g);
+// Loop over every element-local node: CTAs stride over elements (cube
+// coordinates computed once per element), threads over the n^3 local nodes
+// (constant-divisor index math), so consecutive threads touch consecutive
+// addresses.  f(NodeRef, flat index).
+template <int N, class F>
+__device__ __forceinline__ void for_nodes(int side, F&& f) {
+  constexpr int n = N + 1, n3 = n * n * n;
+  const int64_t n_el = int64_t(side) * side * side;
+  for (int64_t e = blockIdx.x; e < n_el; e += gridDim.x) {
+    NodeRef r;
+    r.e = e;
+    r.cz = int(e % side);
+    r.cy = int((e / side) % side);
+    r.cx = int(e / (int64_t(side) * side));
+    for (int l = threadIdx.x; l < n3; l += blockDim.x) {
+      r.i = l % n;
+      r.j = (l / n) % n;
+      r.k = l / (n * n);
+      f(r, e * n3 + l);
+    }
   }
+}
+
+template <int N>
+__global__ void __launch_bounds__(kDssThreads)
+    dss_kernel(const double* __restrict__ in, double* __restrict__ out, int side, int mask) {
+  for_nodes<N>(side, [&](const NodeRef& r, int64_t idx) {
+    out[idx] = (mask && on_boundary<N>(r, side)) ? 0.0 : gather_sum<N>(in, r, side);
+  });
 }
 
 // partials of sum u v / multiplicity (the global inner product of continuous
 // representatives)
+template <int N>
 __global__ void __launch_bounds__(kDssThreads)
-    dot_dss_kernel(const double* __restrict__ u, const double* __restrict__ v, DssGeom g,
+    dot_dss_kernel(const double* __restrict__ u, const double* __restrict__ v, int side,
                    double* __restrict__ part) {
   __shared__ double scratch[kDssThreads / 32];
   double s = 0.0;
-  for (int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < g.ndof;
-       idx += int64_t(gridDim.x) * blockDim.x) {
-    const NodeRef r = decompose(idx, g);
-    s = fma(u[idx], v[idx] / double(node_mult(r, g)), s);
-  }
+  for_nodes<N>(side, [&](const NodeRef& r, int64_t idx) {
+    s = fma(u[idx], v[idx] / double(node_mult<N>(r, side)), s);
+  });
   s = block_sum<kDssThreads>(s, scratch);
   if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
 // alpha = rr / pAp;  x += alpha p;  r -= alpha mask dss(ap);  partials of
 // sum r^2 / multiplicity.  The assembled A p is never written to memory.
+template <int N>
 __global__ void __launch_bounds__(kDssThreads)
     cg_update_dss_kernel(double* __restrict__ x, const double* __restrict__ p,
-                         double* __restrict__ r, const double* __restrict__ ap, DssGeom g,
-                         const double* __restrict__ rr, const double* __restrict__ pap,
-                         double* __restrict__ part) {
+                         double* __restrict__ r, const double* __restrict__ ap, int side,
+                         int mask, const double* __restrict__ rr,
+                         const double* __restrict__ pap, double* __restrict__ part) {
   __shared__ double scratch[kDssThreads / 32];
   const double alpha = rr[0] / pap[0];
   double s = 0.0;
-  for (int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < g.ndof;
-       idx += int64_t(gridDim.x) * blockDim.x) {
-    const NodeRef nr = decompose(idx, g);
-    const double w = (g.mask && on_boundary(nr, g)) ? 0.0 : gather_sum(ap, nr, g);
+  for_nodes<N>(side, [&](const NodeRef& nr, int64_t idx) {
+    const double w = (mask && on_boundary<N>(nr, side)) ? 0.0 : gather_sum<N>(ap, nr, side);
     x[idx] = fma(alpha, p[idx], x[idx]);
     const double ri = fma(-alpha, w, r[idx]);
     r[idx] = ri;
-    s = fma(ri, ri / double(node_mult(nr, g)), s);
-  }
+    s = fma(ri, ri / double(node_mult<N>(nr, side)), s);
+  });
   s = block_sum<kDssThreads>(s, scratch);
   if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
-static int dss_blocks(int64_t n) {
-  const int64_t want = (n + kDssThreads - 1) / kDssThreads;
+static int dss_blocks(int side) {
+  const int64_t n_el = int64_t(side) * side * side;
   const int64_t cap = int64_t(sm_count()) * 8;
-  return int(want < cap ? (want > 0 ? want : 1) : cap);
+  return int(n_el < cap ? n_el : cap);
 }
 
-static DssGeom geom(int side, int degree, int mask) {
-  DssGeom g;
-  g.side = side;
-  g.n = degree + 1;
-  g.n3 = int64_t(g.n) * g.n * g.n;
-  g.ndof = int64_t(side) * side * side * g.n3;
-  g.mask = mask;
-  return g;
-}
+#define HX_DSS_DISPATCH(CALL)                                                   \
+  switch (degree) {                                                            \
+    case 1: CALL(1); case 2: CALL(2); case 3: CALL(3); case 4: CALL(4);        \
+    case 5: CALL(5); case 6: CALL(6); case 7: CALL(7); case 8: CALL(8);        \
+    case 9: CALL(9); case 10: CALL(10); case 11: CALL(11); case 12: CALL(12);  \
+    case 13: CALL(13); case 14: CALL(14); case 15: CALL(15);                   \
+    default: return cudaErrorInvalidValue;                                     \
+  }
 
 cudaError_t launch_dss(const double* in, double* out, int side, int degree, int mask,
                        cudaStream_t s) {
-  const DssGeom g = geom(side, degree, mask);
-  dss_kernel<<<dss_blocks(g.ndof), kDssThreads, 0, s>>>(in, out, g);
+  const int nb = dss_blocks(side);
+#define HX_CALL(N)                                                  \
+  dss_kernel<N><<<nb, kDssThreads, 0, s>>>(in, out, side, mask);   \
   return cudaGetLastError();
+  HX_DSS_DISPATCH(HX_CALL)
+#undef HX_CALL
 }
 
 cudaError_t launch_dot_dss(const double* u, const double* v, int side, int degree,
                            double* part, double* result, cudaStream_t s) {
-  const DssGeom g = geom(side, degree, 0);
-  const int nb = dss_blocks(g.ndof);
-  dot_dss_kernel<<<nb, kDssThreads, 0, s>>>(u, v, g, part);
-  cudaError_t err = cudaGetLastError();
-  if (err != cudaSuccess) return err;
+  const int nb = dss_blocks(side);
+  cudaError_t err;
+#define HX_CALL(N)                                                      \
+  dot_dss_kernel<N><<<nb, kDssThreads, 0, s>>>(u, v, side, part);      \
+  if ((err = cudaGetLastError()) != cudaSuccess) return err;           \
   return launch_sum(part, nb, result, s);
+  HX_DSS_DISPATCH(HX_CALL)
+#undef HX_CALL
 }
 
 cudaError_t launch_cg_update_dss(double* x, const double* p, double* r, const double* ap,
                                  int side, int degree, int mask, const double* rr,
                                  const double* pap, double* part, double* rr_new,
                                  cudaStream_t s) {
-  const DssGeom g = geom(side, degree, mask);
-  const int nb = dss_blocks(g.ndof);
-  cg_update_dss_kernel<<<nb, kDssThreads, 0, s>>>(x, p, r, ap, g, rr, pap, part);
-  cudaError_t err = cudaGetLastError();
-  if (err != cudaSuccess) return err;
+  const int nb = dss_blocks(side);
+  cudaError_t err;
+#define HX_CALL(N)                                                                       \
+  cg_update_dss_kernel<N><<<nb, kDssThreads, 0, s>>>(x, p, r, ap, side, mask, rr, pap,  \
+                                                      part);                            \
+  if ((err = cudaGetLastError()) != cudaSuccess) return err;                            \
   return launch_sum(part, nb, rr_new, s);
+  HX_DSS_DISPATCH(HX_CALL)
+#undef HX_CALL
 }
 
 }  // namespace hx

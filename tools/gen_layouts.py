@@ -21,6 +21,8 @@ strides (``ORD``): with one order per pattern no padding can make both the
 1.86x wavefronts), with k fastest in both it can.
 """
 
+import json
+import os
 import sys
 
 BP1, BP35, BP3 = 10, 35, 30
@@ -30,7 +32,7 @@ TARGET_THREADS = 256
 def lines(d, pat):
     d0, d1, d2 = d
     return {0: (d1 * d2, d0), 1: (d0 * d2, d1), 2: (d0 * d1, d2), 5: (d0 * d1, d2),
-            6: (d0 * d1, d2)}[pat]
+            6: (d0 * d1, d2), 7: (d0 * d2, d1)}[pat]
 
 
 def kofs(lay, k):
@@ -60,6 +62,9 @@ def addr(d, lay, pat, l, t):
         return kofs(lay, t) + j * s1 + i
     if pat == 1:
         k, i = divmod(l, d2)
+        return kofs(lay, k) + t * s1 + i
+    if pat == 7:
+        k, i = pair_coords(l, d0, d2)
         return kofs(lay, k) + t * s1 + i
     if pat == 2:
         k, j = divmod(l, d1)
@@ -97,7 +102,31 @@ def extent(d, lay):
     return kofs(lay, d0 - 1) + (d1 - 1) * lay[1] + d2
 
 
+_CACHE_PATH = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                           "build", "layout_cache.json")
+_cache = None
+
+
 def best_layout(d, pats, paired=False):
+    """Cheapest layout for one tensor phase (memoised in build/ -- the paired
+    search evaluates ~1000 candidates)."""
+    global _cache
+    if _cache is None:
+        try:
+            with open(_CACHE_PATH) as fh:
+                _cache = json.load(fh)
+        except (OSError, ValueError):
+            _cache = {}
+    key = repr((tuple(d), tuple(pats), bool(paired)))
+    if key not in _cache:
+        _cache[key] = list(_best_layout(d, pats, paired))
+        os.makedirs(os.path.dirname(_CACHE_PATH), exist_ok=True)
+        with open(_CACHE_PATH, "w") as fh:
+            json.dump(_cache, fh)
+    return tuple(_cache[key])
+
+
+def _best_layout(d, pats, paired=False):
     d0, d1, d2 = d
     best = None
     for s1 in range(d2, d2 + 4):
@@ -126,9 +155,14 @@ def phases(bp, n, m, ord_=0):
         # orders (k fastest there doubles the L1 tag requests: ncu r09).
         pi = {0: 2, 2: 5, 4: 6}[ord_]
         return [(0, (n, m, n), (1, pi)), (1, (n, m, m), (0, pi))]
-    return [(0, (n, m, n), (1, 2)), (0, (m, m, m), (0, 2)),
-            (1, (n, m, m), (0, 2)), (1, (m, m, m), (0, 1)),
-            (2, (m, m, m), (0, 1, 2)), (2, (n, m, m), (0, 2))]
+    # BP3.0: ORD 4 = k-paired lane order in the i-line stages over the
+    # (n, m, .) tensors (S2, S8: pattern 6).  The (m, m, m) stages S4 / S6 keep
+    # theirs: with odd m the unpaired last slice costs more than it saves
+    # (r11: 1.3-1.5x wavefronts there with pattern 6 / 7).
+    pi = 6 if ord_ == 4 else 2
+    return [(0, (n, m, n), (1, pi)), (0, (m, m, m), (0, 2)),
+            (1, (n, m, m), (0, pi)), (1, (m, m, m), (0, 1)),
+            (2, (m, m, m), (0, 1, 2)), (2, (n, m, m), (0, pi))]
 
 
 def q_stage_stride(n):
@@ -157,11 +191,14 @@ def plan(bp, deg, target=TARGET_THREADS, qstage=False):
         # BP1.0 only: a CTA smaller than one element's line count walks over
         # the lines (for_lines); one element per tile
         nt = max(32, -(-target // 32) * 32)
-    ords = (0, 2, 4) if bp == BP1 else (0,)
+    # BP3.0 supports ORD 4 too, but it measured 1-2 % slower at N=7 despite
+    # fewer conflicts (r11/r12: latency-bound, not shared-memory-bound), so
+    # the search stays on the default order there
+    ords = {BP1: (0, 2, 4)}.get(bp, (0,))
     best = None
     for o in ords:  # BP1.0: lane orders chosen jointly with the strides
         ph_o = phases(bp, n, m, o)
-        lays_o = [best_layout(d, pats, paired=(o == 4)) for _, d, pats in ph_o]
+        lays_o = [best_layout(d, pats, paired=(6 in pats or 7 in pats)) for _, d, pats in ph_o]
         c = sum(cost(d, lay, pats, 1, 0) for (_, d, pats), lay in zip(ph_o, lays_o))
         if best is None or c < best[0]:
             best = (c, o, ph_o, lays_o)
