@@ -133,23 +133,30 @@ int hx_cg_direction(double* p, const double* r, int64_t n, const double* rr_new,
 
 /* Assembly on the structured cube mesh of build_cube_mesh(side, extent)
  * (mesh.py:44-56; element e = (cx*side + cy)*side + cz, local (k,j,i) is
- * global node (cx N + i, cy N + j, cz N + k)); vectors are element-local,
- * side^3 * (degree+1)^3 doubles.  New: the reference has no assembly
- * (SPEC.md:220); this serves the assembled CG solve.
+ * global node (cx N + i, cy N + j, cz N + k)).  New: the reference has no
+ * assembly; this serves the assembled CG solve.
+ * Each call processes the elements [e_begin, e_end) (a rank's shard; 0 and
+ * side^3 on one GPU).  Own vectors (out, u, v, x, p, r) hold exactly those
+ * elements; the GATHERED vector (in, ap) holds elements from `*_base` on and
+ * must include every element that shares a node with the range (at most
+ * side^2 + side + 1 elements beyond either end: the halo).
  *   hx_dss:           out = mask . Q Q^T in  (sum over the copies of each
  *                     global node, canonical order: bitwise deterministic;
  *                     mask_boundary zeroes the cube-boundary nodes)
- *   hx_dot_dss:       *result = sum u v / multiplicity  (= <u_G, v_G> for
- *                     continuous representatives)
+ *   hx_dot_dss:       *result = sum u v / multiplicity over the range
+ *                     (= <u_G, v_G> for continuous representatives, summed
+ *                     over ranks)
  *   hx_cg_update_dss: hx_cg_update with r -= alpha mask Q Q^T ap and the
  *                     multiplicity-weighted <r, r>                             */
 int hx_dss(const double* in, double* out, int side, int degree, int mask_boundary,
-           void* stream);
-int hx_dot_dss(const double* u, const double* v, int side, int degree, double* partials,
-               int64_t n_partials, double* result, void* stream);
+           int64_t e_begin, int64_t e_end, int64_t in_base, void* stream);
+int hx_dot_dss(const double* u, const double* v, int side, int degree, int64_t e_begin,
+               int64_t e_end, double* partials, int64_t n_partials, double* result,
+               void* stream);
 int hx_cg_update_dss(double* x, const double* p, double* r, const double* ap, int side,
-                     int degree, int mask_boundary, const double* rr, const double* pap,
-                     double* partials, int64_t n_partials, double* rr_new, void* stream);
+                     int degree, int mask_boundary, int64_t e_begin, int64_t e_end,
+                     int64_t ap_base, const double* rr, const double* pap, double* partials,
+                     int64_t n_partials, double* rr_new, void* stream);
 
 /* Elements each CTA processes per tile, threads per CTA and dynamic shared
  * memory bytes of the plan's kernel (for reports and tests).                */

@@ -208,3 +208,17 @@ def assembled_cg(apply, b, side, degree, mask, tol=1e-13, maxiter=2000):
         p = r + rn / rr * p
         rr = rn
     return x, maxiter
+
+
+def dss_range(pad, side, degree, e_begin, e_end, base, mask=False):
+    """mask . Q Q^T restricted to elements [e_begin, e_end), computed ONLY from
+    the padded vector ``pad`` holding elements [base, base + len(pad)) -- the
+    rank-local view of csrc/hx_dss.cu's range semantics (checks that the halo
+    holds every copy of every own node)."""
+    gidx = cube_global_index(side, degree)
+    ng = (side * degree + 1) ** 3
+    top = base + pad.shape[0]
+    s = scatter_add(pad, gidx[base:top], ng)
+    if mask:
+        s[cube_boundary(side, degree)] = 0.0
+    return s[gidx[e_begin:e_end]]

@@ -147,115 +147,204 @@ def cg_iterations(op, b, iterations, work, stream=None):
 # element-local copies.  On the build_cube_mesh(side, extent) numbering
 # (mesh.py:44-56) Q Q^T is a fixed-order gather (hx_dss), and CG runs on
 # continuous element-local representatives (see csrc/hx_dss.cu).
+#
+# Multi-GPU: rank r owns the reference chunking's element range [lo, hi)
+# (shard.partition).  The gathered vector (A p) additionally needs the
+# elements that share a node with the range -- at most side^2 + side + 1
+# either side, owned by the neighbouring ranks -- so each iteration exchanges
+# those halos with the two neighbours (point-to-point send/recv, NCCL over
+# NVLink on GPUs) between the matvec and the update kernel.  Every copy of a
+# shared node then sums the same values in the same order on every rank, so
+# the ranks' representatives stay bitwise consistent.
 
 
-def gather_scatter(u, side, degree, mask_boundary=False, out=None, stream=None):
+def _check_cube(u, n_el, degree):
+    if u.numel() != n_el * (degree + 1) ** 3:
+        raise ValueError(f"vector has {u.numel()} entries, expected {n_el} elements of "
+                         f"{(degree + 1) ** 3} nodes")
+
+
+class AssembledShard:
+    """This rank's piece of the assembled cube-mesh system: own elements
+    [lo, hi) plus the halo range [base, top) the gather-scatter reads."""
+
+    def __init__(self, side, degree, rank=0, world_size=1, group=None):
+        from .shard import partition
+
+        self.side, self.degree = side, degree
+        self.rank, self.world_size, self.group = rank, world_size, group
+        n_el = side ** 3
+        parts = partition(n_el, world_size)
+        self.lo, self.hi = parts[rank]
+        self.halo = side * side + side + 1
+        if world_size > 1 and min(h - l for l, h in parts) < self.halo:
+            raise ValueError(f"every rank needs >= side^2 + side + 1 = {self.halo} elements "
+                             f"(the halo must come from the direct neighbours)")
+        self.base = max(0, self.lo - self.halo)
+        self.top = min(n_el, self.hi + self.halo)
+        self.n_own = self.hi - self.lo
+        self.n_pad = self.top - self.base
+
+    def padded(self, like):
+        """Zeroed (n_pad, n_p) buffer on like's device."""
+        import torch
+        return torch.zeros((self.n_pad, like.shape[-1]), dtype=like.dtype, device=like.device)
+
+    def own(self, pad):
+        """View of the own elements inside a padded buffer."""
+        return pad[self.lo - self.base: self.hi - self.base]
+
+    def exchange(self, pad):
+        """Fill the halo rows of ``pad`` from the neighbouring ranks (their own
+        rows), sending ours to them.  No-op on one rank."""
+        if self.world_size == 1:
+            return
+        import torch.distributed as dist
+
+        ops = []
+        o0, o1 = self.lo - self.base, self.hi - self.base
+        if self.rank > 0:  # halo below: [base, lo) belongs to rank - 1
+            ops.append(dist.P2POp(dist.irecv, pad[:o0], self.rank - 1, self.group))
+            n_send = min(self.halo, self.n_own)
+            ops.append(dist.P2POp(dist.isend, pad[o0:o0 + n_send].contiguous(), self.rank - 1,
+                                  self.group))
+        if self.rank < self.world_size - 1:  # halo above: [hi, top) belongs to rank + 1
+            ops.append(dist.P2POp(dist.irecv, pad[o1:], self.rank + 1, self.group))
+            n_send = min(self.halo, self.n_own)
+            ops.append(dist.P2POp(dist.isend, pad[o1 - n_send:o1].contiguous(), self.rank + 1,
+                                  self.group))
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+
+
+def gather_scatter(u, side, degree, mask_boundary=False, out=None, stream=None, shard=None):
     """``out = mask . Q Q^T u`` on device: every element-local copy of a global
-    node receives the (bit-identical) sum over all its copies."""
+    node receives the (bit-identical) sum over all its copies.  With a
+    ``shard``, ``u`` is the rank's padded buffer (halos already exchanged)
+    and ``out`` covers the own elements."""
     import torch
 
+    sh = shard or AssembledShard(side, degree)
+    _check_cube(u, sh.n_pad, degree)
     if out is None:
-        out = torch.empty_like(u)
-    _check_cube(u, side, degree)
+        out = torch.empty((sh.n_own, u.shape[-1]), dtype=u.dtype, device=u.device)
     stream = _stream(u.device) if stream is None else stream
     _native.check(_native.lib().hx_dss(_native.ptr(u), _native.ptr(out), side, degree,
-                                       int(bool(mask_boundary)), stream), "hx_dss")
+                                       int(bool(mask_boundary)), sh.lo, sh.hi, sh.base,
+                                       stream), "hx_dss")
     return out
 
 
-def _check_cube(u, side, degree):
-    if u.numel() != side ** 3 * (degree + 1) ** 3:
-        raise ValueError(f"vector has {u.numel()} entries, the side-{side} cube mesh at degree "
-                         f"{degree} has {side ** 3 * (degree + 1) ** 3}")
+def _global_sum(t, sh):
+    if sh.world_size > 1:
+        _allreduce(t, sh.group)
+
+
+class _AssembledState:
+    def __init__(self, op, side, b, mask_boundary, work, shard):
+        import torch
+
+        self.sh = shard or AssembledShard(side, op.degree)
+        if op.n_el != self.sh.n_own:
+            raise ValueError("operator does not cover this rank's element range")
+        _check_cube(b, self.sh.n_own, op.degree)
+        self.mask = int(bool(mask_boundary))
+        self.w = work if work is not None else CGWorkspace(b)
+        self.ap_pad = self.sh.padded(b)      # A p with halos
+        self.x = torch.zeros_like(b)
+
+
+def _assembled_setup(op, side, b, st, stream):
+    """r = mask dss(b) (b exchanged through the halo buffer), p = r, <r, r>."""
+    L, ptr, sh, w = _native.lib(), _native.ptr, st.sh, st.w
+    sh.own(st.ap_pad).copy_(b)
+    sh.exchange(st.ap_pad)
+    gather_scatter(st.ap_pad, side, op.degree, st.mask, out=w.r, stream=stream, shard=sh)
+    w.p.copy_(w.r)
+    _native.check(L.hx_dot_dss(ptr(w.r), ptr(w.r), side, op.degree, sh.lo, sh.hi,
+                               ptr(w.partials), w.npart, ptr(w.rr[0]), stream), "hx_dot_dss")
+    _global_sum(w.rr[0], sh)
+
+
+def _assembled_step(op, side, st, cur, stream, flag=None):
+    """One CG iteration; returns the index of the new <r, r> slot."""
+    L, ptr, sh, w = _native.lib(), _native.ptr, st.sh, st.w
+    nxt = 1 - cur
+    ap_own = sh.own(st.ap_pad)
+    _native.check(L.hx_apply_energy(op.plan.handle, ptr(w.p), ptr(op.device_factors),
+                                    ptr(ap_own), op.n_el, ptr(w.partials), w.npart, ptr(w.pap),
+                                    ptr(flag), stream), "hx_apply_energy")
+    _global_sum(w.pap, sh)
+    sh.exchange(st.ap_pad)
+    _native.check(L.hx_cg_update_dss(ptr(st.x), ptr(w.p), ptr(w.r), ptr(st.ap_pad), side,
+                                     op.degree, st.mask, sh.lo, sh.hi, sh.base, ptr(w.rr[cur]),
+                                     ptr(w.pap), ptr(w.partials), w.npart, ptr(w.rr[nxt]),
+                                     stream), "hx_cg_update_dss")
+    _global_sum(w.rr[nxt], sh)
+    return nxt
 
 
 def cg_solve_assembled(op, side, b, tol=1e-10, maxiter=1000, check_every=10,
-                       mask_boundary=True, work=None):
+                       mask_boundary=True, work=None, shard=None):
     """Solve the assembled system ``mask Q^T A_L Q x = mask Q^T b`` by CG.
 
     ``op`` is an OperatorInstance on build_cube_mesh(side, extent) (perturbing
-    the corners breaks conformity, so use the unperturbed mesh); ``b`` is an
-    element-local load vector (for instance the BP1.0 mass matvec of a nodal
-    source).  Boundary nodes carry homogeneous Dirichlet conditions when
-    ``mask_boundary`` (needed for BP3.5 / BP3.0 with lam = 0).  Returns a
-    CGResult whose ``x`` is continuous (every copy of a global node holds the
-    same value).  Per iteration: the fused matvec + <p, A p>, then one update
-    kernel that gathers A p across element copies on the fly (the assembled
-    vector is never stored), then the direction update.
+    the corners breaks conformity, so use the unperturbed mesh) -- or, with a
+    ``shard`` (AssembledShard), this rank's ShardedOperator.op on its element
+    range; ``b`` is the (rank's) element-local load vector, e.g. the BP1.0
+    mass matvec of a nodal source.  Boundary nodes carry homogeneous Dirichlet
+    conditions when ``mask_boundary`` (needed for BP3.5 / BP3.0 with
+    lam = 0).  Returns a CGResult whose ``x`` is continuous (every copy of a
+    global node holds the same value).  Per iteration: the fused matvec +
+    <p, A p>, the halo exchange (multi-GPU), one update kernel that gathers
+    A p across element copies on the fly (the assembled vector is never
+    stored), the direction update.
     """
     import torch
 
-    L = _native.lib()
-    ptr = _native.ptr
-    deg = op.degree
-    _check_cube(b, side, deg)
-    if op.n_el != side ** 3:
-        raise ValueError("operator mesh is not the side^3 cube mesh")
     dev = op.device
     stream = _stream(dev)
-    n = b.numel()
-    mask = int(bool(mask_boundary))
-    w = work if work is not None else CGWorkspace(b)
-    x = torch.zeros_like(b)
+    st = _AssembledState(op, side, b, mask_boundary, work, shard)
+    w = st.w
     flag = torch.zeros(1, dtype=torch.int32, device=dev)
-
-    gather_scatter(b, side, deg, mask_boundary, out=w.r, stream=stream)
-    w.p.copy_(w.r)
-    cur = 0
-    _native.check(L.hx_dot_dss(ptr(w.r), ptr(w.r), side, deg, ptr(w.partials), w.npart,
-                               ptr(w.rr[cur]), stream), "hx_dot_dss")
-    target = tol * float(w.rr[cur].sqrt().item())
-    norms = [float(w.rr[cur].sqrt().item())]
-    if norms[0] == 0.0:
-        return CGResult(x, 0, True, norms)
-    it = 0
-    converged = False
+    _assembled_setup(op, side, b, st, stream)
+    norm0 = float(w.rr[0].sqrt().item())
+    target = tol * norm0
+    norms = [norm0]
+    if norm0 == 0.0:
+        return CGResult(st.x, 0, True, norms)
+    it, cur, converged = 0, 0, False
+    n = b.numel()
     while it < maxiter:
-        nxt = 1 - cur
-        _native.check(L.hx_apply_energy(op.plan.handle, ptr(w.p), ptr(op.device_factors),
-                                        ptr(w.ap), op.n_el, ptr(w.partials), w.npart,
-                                        ptr(w.pap), ptr(flag), stream), "hx_apply_energy")
-        _native.check(L.hx_cg_update_dss(ptr(x), ptr(w.p), ptr(w.r), ptr(w.ap), side, deg, mask,
-                                         ptr(w.rr[cur]), ptr(w.pap), ptr(w.partials), w.npart,
-                                         ptr(w.rr[nxt]), stream), "hx_cg_update_dss")
+        nxt = _assembled_step(op, side, st, cur, stream, flag)
         it += 1
         if it % check_every == 0 or it == maxiter:
             norms.append(float(w.rr[nxt].sqrt().item()))
             if norms[-1] <= target:
                 converged = True
                 break
-        _native.check(L.hx_cg_direction(ptr(w.p), ptr(w.r), n, ptr(w.rr[nxt]), ptr(w.rr[cur]),
-                                        stream), "hx_cg_direction")
+        _native.check(_native.lib().hx_cg_direction(_native.ptr(w.p), _native.ptr(w.r), n,
+                                                    _native.ptr(w.rr[nxt]),
+                                                    _native.ptr(w.rr[cur]), stream),
+                      "hx_cg_direction")
         cur = nxt
     if int(flag.item()) & _native.HX_FLAG_NONFINITE:
         raise ValueError("non-finite values during the CG solve")
-    return CGResult(x, it, converged, norms)
+    return CGResult(st.x, it, converged, norms)
 
 
-def cg_iterations_assembled(op, side, b, iterations, work, mask_boundary=True, stream=None):
+def cg_iterations_assembled(op, side, b, iterations, work, mask_boundary=True, shard=None):
     """``iterations`` assembled-CG steps from x = 0 with no convergence checks
     or host synchronisation (the harness times this)."""
-    import torch
-
-    L = _native.lib()
-    ptr = _native.ptr
-    deg = op.degree
-    n = b.numel()
-    stream = _stream(op.device) if stream is None else stream
-    mask = int(bool(mask_boundary))
-    x = torch.zeros_like(b)
-    w = work
-    gather_scatter(b, side, deg, mask_boundary, out=w.r, stream=stream)
-    w.p.copy_(w.r)
+    stream = _stream(op.device)
+    st = _AssembledState(op, side, b, mask_boundary, work, shard)
+    _assembled_setup(op, side, b, st, stream)
     cur = 0
-    L.hx_dot_dss(ptr(w.r), ptr(w.r), side, deg, ptr(w.partials), w.npart, ptr(w.rr[cur]), stream)
+    n = b.numel()
+    w = st.w
     for _ in range(iterations):
-        nxt = 1 - cur
-        L.hx_apply_energy(op.plan.handle, ptr(w.p), ptr(op.device_factors), ptr(w.ap),
-                          op.n_el, ptr(w.partials), w.npart, ptr(w.pap), None, stream)
-        L.hx_cg_update_dss(ptr(x), ptr(w.p), ptr(w.r), ptr(w.ap), side, deg, mask,
-                           ptr(w.rr[cur]), ptr(w.pap), ptr(w.partials), w.npart,
-                           ptr(w.rr[nxt]), stream)
-        L.hx_cg_direction(ptr(w.p), ptr(w.r), n, ptr(w.rr[nxt]), ptr(w.rr[cur]), stream)
+        nxt = _assembled_step(op, side, st, cur, stream)
+        _native.lib().hx_cg_direction(_native.ptr(w.p), _native.ptr(w.r), n,
+                                      _native.ptr(w.rr[nxt]), _native.ptr(w.rr[cur]), stream)
         cur = nxt
-    return x
+    return st.x

@@ -299,33 +299,43 @@ int hx_cg_direction(double* p, const double* r, int64_t n, const double* rr_new,
                                          static_cast<cudaStream_t>(stream)));
 }
 
-static bool dss_args_ok(int side, int degree) {
-  return side >= 1 && side <= 4096 && degree >= 1 && degree <= 15;
+static bool dss_args_ok(int side, int degree, int64_t e_begin, int64_t e_end) {
+  return side >= 1 && side <= 4096 && degree >= 1 && degree <= 15 && e_begin >= 0 &&
+         e_begin <= e_end && e_end <= int64_t(side) * side * side;
 }
 
-int hx_dss(const double* in, double* out, int side, int degree, int mask, void* stream) {
-  if (!dss_args_ok(side, degree) || !in || !out || in == out) return HX_EINVAL;
-  return cuda_status(launch_dss(in, out, side, degree, mask != 0,
+int hx_dss(const double* in, double* out, int side, int degree, int mask, int64_t e_begin,
+           int64_t e_end, int64_t in_base, void* stream) {
+  if (!dss_args_ok(side, degree, e_begin, e_end) || in_base < 0 || in_base > e_begin)
+    return HX_EINVAL;
+  if (e_end == e_begin) return HX_OK;
+  if (!in || !out || in == out) return HX_EINVAL;
+  return cuda_status(launch_dss(in, out, side, degree, mask != 0, e_begin, e_end, in_base,
                                 static_cast<cudaStream_t>(stream)));
 }
 
-int hx_dot_dss(const double* u, const double* v, int side, int degree, double* partials,
-               int64_t n_partials, double* result, void* stream) {
-  if (!dss_args_ok(side, degree) || !u || !v || !partials || !result) return HX_EINVAL;
+int hx_dot_dss(const double* u, const double* v, int side, int degree, int64_t e_begin,
+               int64_t e_end, double* partials, int64_t n_partials, double* result,
+               void* stream) {
+  if (!dss_args_ok(side, degree, e_begin, e_end) || !partials || !result) return HX_EINVAL;
+  if (e_end > e_begin && (!u || !v)) return HX_EINVAL;
   if (n_partials < hx_energy_partials()) return HX_EINVAL;
-  return cuda_status(launch_dot_dss(u, v, side, degree, partials, result,
+  return cuda_status(launch_dot_dss(u, v, side, degree, e_begin, e_end, partials, result,
                                     static_cast<cudaStream_t>(stream)));
 }
 
 int hx_cg_update_dss(double* x, const double* p, double* r, const double* ap, int side,
-                     int degree, int mask, const double* rr, const double* pap,
-                     double* partials, int64_t n_partials, double* rr_new, void* stream) {
-  if (!dss_args_ok(side, degree) || !x || !p || !r || !ap || !rr || !pap || !partials ||
-      !rr_new)
+                     int degree, int mask, int64_t e_begin, int64_t e_end, int64_t ap_base,
+                     const double* rr, const double* pap, double* partials,
+                     int64_t n_partials, double* rr_new, void* stream) {
+  if (!dss_args_ok(side, degree, e_begin, e_end) || ap_base < 0 || ap_base > e_begin)
     return HX_EINVAL;
+  if (!rr || !pap || !partials || !rr_new) return HX_EINVAL;
+  if (e_end > e_begin && (!x || !p || !r || !ap)) return HX_EINVAL;
   if (n_partials < hx_energy_partials()) return HX_EINVAL;
-  return cuda_status(launch_cg_update_dss(x, p, r, ap, side, degree, mask != 0, rr, pap,
-                                          partials, rr_new, static_cast<cudaStream_t>(stream)));
+  return cuda_status(launch_cg_update_dss(x, p, r, ap, side, degree, mask != 0, e_begin, e_end,
+                                          ap_base, rr, pap, partials, rr_new,
+                                          static_cast<cudaStream_t>(stream)));
 }
 
 int hx_measure_smem_bandwidth(double* bytes_per_s, void* stream) {

@@ -15,6 +15,12 @@
 // is deterministic -- no atomics.  With `mask`, nodes on the cube boundary are
 // zeroed (homogeneous Dirichlet conditions).
 //
+// Element ranges (multi-GPU): a rank owns elements [e_begin, e_end) of the
+// cube; its own vectors start at e_begin, while the vector that is gathered
+// (the one dss sums) starts at element `base` <= e_begin and must also hold
+// every element sharing a node with the range -- at most side^2 + side + 1
+// elements either side, filled by a halo exchange (cg.AssembledShard).
+//
 // Assembled CG keeps every vector in element-local storage as its continuous
 // representative u_L = Q u_G.  Then
 //   <p_G, A_G p_G> = <p_L, A_L p_L>                 (fused into the matvec)
@@ -46,6 +52,12 @@ __device__ __forceinline__ AxisCopies axis_copies(int c, int i, int side, int N)
   return a;
 }
 
+struct DssRange {
+  int side;
+  int64_t e_begin, e_end;  // elements processed (own vectors start at e_begin)
+  int64_t base;            // first element of the gathered vector
+};
+
 // One element-local node: its element (and that element's cube coordinates,
 // computed once per element by the caller) and its (k, j, i).
 struct NodeRef {
@@ -60,60 +72,72 @@ __device__ __forceinline__ bool on_boundary(const NodeRef& r, int side) {
   return gx == 0 || gx == G || gy == 0 || gy == G || gz == 0 || gz == G;
 }
 
-// number of element-local copies of node r
+// 1 / (number of element-local copies of node r): 1, 1/2, 1/4 or 1/8, so
+// scaling by it is exact (same bits as dividing by the count)
 template <int N>
-__device__ __forceinline__ int node_mult(const NodeRef& r, int side) {
-  return axis_copies(r.cx, r.i, side, N).cnt * axis_copies(r.cy, r.j, side, N).cnt *
-         axis_copies(r.cz, r.k, side, N).cnt;
+__device__ __forceinline__ double inv_mult(const NodeRef& r, int side) {
+  const int c = axis_copies(r.cx, r.i, side, N).cnt + axis_copies(r.cy, r.j, side, N).cnt +
+                axis_copies(r.cz, r.k, side, N).cnt - 3;  // log2 of the count
+  return c == 0 ? 1.0 : c == 1 ? 0.5 : c == 2 ? 0.25 : 0.125;
 }
 
-// sum over the copies of node r, in the canonical order
+// sum over the copies of node r, in the canonical order (x outer, z inner,
+// each ascending); bounded loops with predicates, no dynamic trip counts
 template <int N>
 __device__ __forceinline__ double gather_sum(const double* __restrict__ u, const NodeRef& r,
-                                             int side) {
+                                             int side, int64_t base) {
   constexpr int n = N + 1, n3 = n * n * n;
   const AxisCopies ax = axis_copies(r.cx, r.i, side, N);
   const AxisCopies ay = axis_copies(r.cy, r.j, side, N);
   const AxisCopies az = axis_copies(r.cz, r.k, side, N);
   const int64_t s = side;
   double sum = 0.0;
-  for (int a = 0; a < ax.cnt; ++a)
-    for (int b = 0; b < ay.cnt; ++b)
-      for (int c = 0; c < az.cnt; ++c) {
+#pragma unroll
+  for (int a = 0; a < 2; ++a) {
+    if (a >= ax.cnt) break;
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      if (b >= ay.cnt) break;
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        if (c >= az.cnt) break;
         const int64_t e = r.e + ax.d[a] * s * s + ay.d[b] * s + az.d[c];
-        sum += u[e * n3 + (az.l[c] * n + ay.l[b]) * n + ax.l[a]];
+        sum += u[(e - base) * n3 + (az.l[c] * n + ay.l[b]) * n + ax.l[a]];
       }
+    }
+  }
   return sum;
 }
 
-// Loop over every element-local node: CTAs stride over elements (cube
-// coordinates computed once per element), threads over the n^3 local nodes
-// (constant-divisor index math), so consecutive threads touch consecutive
-// addresses.  f(NodeRef, flat index).
+// Loop over every element-local node of the range: CTAs stride over
+// elements (cube coordinates computed once per element), threads over the
+// n^3 local nodes (constant-divisor index math), so consecutive threads touch
+// consecutive addresses.  f(NodeRef, index into the range's own vectors).
 template <int N, class F>
-__device__ __forceinline__ void for_nodes(int side, F&& f) {
+__device__ __forceinline__ void for_nodes(const DssRange& g, F&& f) {
   constexpr int n = N + 1, n3 = n * n * n;
-  const int64_t n_el = int64_t(side) * side * side;
-  for (int64_t e = blockIdx.x; e < n_el; e += gridDim.x) {
+  const int64_t side = g.side;
+  for (int64_t e = g.e_begin + blockIdx.x; e < g.e_end; e += gridDim.x) {
     NodeRef r;
     r.e = e;
     r.cz = int(e % side);
     r.cy = int((e / side) % side);
-    r.cx = int(e / (int64_t(side) * side));
+    r.cx = int(e / (side * side));
+    const int64_t own = (e - g.e_begin) * n3;
     for (int l = threadIdx.x; l < n3; l += blockDim.x) {
       r.i = l % n;
       r.j = (l / n) % n;
       r.k = l / (n * n);
-      f(r, e * n3 + l);
+      f(r, own + l);
     }
   }
 }
 
 template <int N>
 __global__ void __launch_bounds__(kDssThreads)
-    dss_kernel(const double* __restrict__ in, double* __restrict__ out, int side, int mask) {
-  for_nodes<N>(side, [&](const NodeRef& r, int64_t idx) {
-    out[idx] = (mask && on_boundary<N>(r, side)) ? 0.0 : gather_sum<N>(in, r, side);
+    dss_kernel(const double* __restrict__ in, double* __restrict__ out, DssRange g, int mask) {
+  for_nodes<N>(g, [&](const NodeRef& r, int64_t idx) {
+    out[idx] = (mask && on_boundary<N>(r, g.side)) ? 0.0 : gather_sum<N>(in, r, g.side, g.base);
   });
 }
 
@@ -121,12 +145,12 @@ __global__ void __launch_bounds__(kDssThreads)
 // representatives)
 template <int N>
 __global__ void __launch_bounds__(kDssThreads)
-    dot_dss_kernel(const double* __restrict__ u, const double* __restrict__ v, int side,
+    dot_dss_kernel(const double* __restrict__ u, const double* __restrict__ v, DssRange g,
                    double* __restrict__ part) {
   __shared__ double scratch[kDssThreads / 32];
   double s = 0.0;
-  for_nodes<N>(side, [&](const NodeRef& r, int64_t idx) {
-    s = fma(u[idx], v[idx] / double(node_mult<N>(r, side)), s);
+  for_nodes<N>(g, [&](const NodeRef& r, int64_t idx) {
+    s = fma(u[idx], v[idx] * inv_mult<N>(r, g.side), s);
   });
   s = block_sum<kDssThreads>(s, scratch);
   if (threadIdx.x == 0) part[blockIdx.x] = s;
@@ -137,27 +161,28 @@ __global__ void __launch_bounds__(kDssThreads)
 template <int N>
 __global__ void __launch_bounds__(kDssThreads)
     cg_update_dss_kernel(double* __restrict__ x, const double* __restrict__ p,
-                         double* __restrict__ r, const double* __restrict__ ap, int side,
+                         double* __restrict__ r, const double* __restrict__ ap, DssRange g,
                          int mask, const double* __restrict__ rr,
                          const double* __restrict__ pap, double* __restrict__ part) {
   __shared__ double scratch[kDssThreads / 32];
   const double alpha = rr[0] / pap[0];
   double s = 0.0;
-  for_nodes<N>(side, [&](const NodeRef& nr, int64_t idx) {
-    const double w = (mask && on_boundary<N>(nr, side)) ? 0.0 : gather_sum<N>(ap, nr, side);
+  for_nodes<N>(g, [&](const NodeRef& nr, int64_t idx) {
+    const double w =
+        (mask && on_boundary<N>(nr, g.side)) ? 0.0 : gather_sum<N>(ap, nr, g.side, g.base);
     x[idx] = fma(alpha, p[idx], x[idx]);
     const double ri = fma(-alpha, w, r[idx]);
     r[idx] = ri;
-    s = fma(ri, ri / double(node_mult<N>(nr, side)), s);
+    s = fma(ri, ri * inv_mult<N>(nr, g.side), s);
   });
   s = block_sum<kDssThreads>(s, scratch);
   if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
-static int dss_blocks(int side) {
-  const int64_t n_el = int64_t(side) * side * side;
+static int dss_blocks(const DssRange& g) {
+  const int64_t n_el = g.e_end - g.e_begin;
   const int64_t cap = int64_t(sm_count()) * 8;
-  return int(n_el < cap ? n_el : cap);
+  return int(n_el < 1 ? 1 : (n_el < cap ? n_el : cap));
 }
 
 #define HX_DSS_DISPATCH(CALL)                                                   \
@@ -169,38 +194,51 @@ static int dss_blocks(int side) {
     default: return cudaErrorInvalidValue;                                     \
   }
 
+static DssRange range(int side, int64_t e_begin, int64_t e_end, int64_t base) {
+  DssRange g;
+  g.side = side;
+  g.e_begin = e_begin;
+  g.e_end = e_end;
+  g.base = base;
+  return g;
+}
+
 cudaError_t launch_dss(const double* in, double* out, int side, int degree, int mask,
-                       cudaStream_t s) {
-  const int nb = dss_blocks(side);
-#define HX_CALL(N)                                                  \
-  dss_kernel<N><<<nb, kDssThreads, 0, s>>>(in, out, side, mask);   \
+                       int64_t e_begin, int64_t e_end, int64_t base, cudaStream_t s) {
+  const DssRange g = range(side, e_begin, e_end, base);
+  const int nb = dss_blocks(g);
+#define HX_CALL(N)                                              \
+  dss_kernel<N><<<nb, kDssThreads, 0, s>>>(in, out, g, mask);  \
   return cudaGetLastError();
   HX_DSS_DISPATCH(HX_CALL)
 #undef HX_CALL
 }
 
 cudaError_t launch_dot_dss(const double* u, const double* v, int side, int degree,
-                           double* part, double* result, cudaStream_t s) {
-  const int nb = dss_blocks(side);
+                           int64_t e_begin, int64_t e_end, double* part, double* result,
+                           cudaStream_t s) {
+  const DssRange g = range(side, e_begin, e_end, e_begin);
+  const int nb = dss_blocks(g);
   cudaError_t err;
-#define HX_CALL(N)                                                      \
-  dot_dss_kernel<N><<<nb, kDssThreads, 0, s>>>(u, v, side, part);      \
-  if ((err = cudaGetLastError()) != cudaSuccess) return err;           \
+#define HX_CALL(N)                                                 \
+  dot_dss_kernel<N><<<nb, kDssThreads, 0, s>>>(u, v, g, part);    \
+  if ((err = cudaGetLastError()) != cudaSuccess) return err;      \
   return launch_sum(part, nb, result, s);
   HX_DSS_DISPATCH(HX_CALL)
 #undef HX_CALL
 }
 
 cudaError_t launch_cg_update_dss(double* x, const double* p, double* r, const double* ap,
-                                 int side, int degree, int mask, const double* rr,
+                                 int side, int degree, int mask, int64_t e_begin,
+                                 int64_t e_end, int64_t ap_base, const double* rr,
                                  const double* pap, double* part, double* rr_new,
                                  cudaStream_t s) {
-  const int nb = dss_blocks(side);
+  const DssRange g = range(side, e_begin, e_end, ap_base);
+  const int nb = dss_blocks(g);
   cudaError_t err;
-#define HX_CALL(N)                                                                       \
-  cg_update_dss_kernel<N><<<nb, kDssThreads, 0, s>>>(x, p, r, ap, side, mask, rr, pap,  \
-                                                      part);                            \
-  if ((err = cudaGetLastError()) != cudaSuccess) return err;                            \
+#define HX_CALL(N)                                                                            \
+  cg_update_dss_kernel<N><<<nb, kDssThreads, 0, s>>>(x, p, r, ap, g, mask, rr, pap, part);   \
+  if ((err = cudaGetLastError()) != cudaSuccess) return err;                                 \
   return launch_sum(part, nb, rr_new, s);
   HX_DSS_DISPATCH(HX_CALL)
 #undef HX_CALL

@@ -57,11 +57,13 @@ cudaError_t launch_cg_direction(double* p, const double* r, int64_t n, const dou
                                 const double* rr_old, cudaStream_t s);
 
 cudaError_t launch_dss(const double* in, double* out, int side, int degree, int mask,
-                       cudaStream_t s);
+                       int64_t e_begin, int64_t e_end, int64_t base, cudaStream_t s);
 cudaError_t launch_dot_dss(const double* u, const double* v, int side, int degree,
-                           double* part, double* result, cudaStream_t s);
+                           int64_t e_begin, int64_t e_end, double* part, double* result,
+                           cudaStream_t s);
 cudaError_t launch_cg_update_dss(double* x, const double* p, double* r, const double* ap,
-                                 int side, int degree, int mask, const double* rr,
+                                 int side, int degree, int mask, int64_t e_begin,
+                                 int64_t e_end, int64_t ap_base, const double* rr,
                                  const double* pap, double* part, double* rr_new,
                                  cudaStream_t s);
 

@@ -72,3 +72,54 @@ def test_gloo_world2_gather_and_dot(tmp_path):
     # element-local operator: sharded and gathered == one shot, bit for bit
     np.testing.assert_array_equal(res["full"], ref)
     assert abs(float(res["dot"][0]) - float(np.sum(q * ref))) <= 1e-12 * abs(float(np.sum(q * ref)))
+
+
+def _halo_worker(rank, world, port, result_path):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import hexbench_oracle as orc
+        from paper_1711_00903_b200.cg import AssembledShard
+
+        side, deg = 4, 2
+        n3 = (deg + 1) ** 3
+        u = np.random.default_rng(5).standard_normal((side ** 3, n3))
+        sh = AssembledShard(side, deg, rank, world)
+        pad = sh.padded(torch.zeros(1, n3, dtype=torch.float64))
+        sh.own(pad).copy_(torch.from_numpy(u[sh.lo:sh.hi]))
+        sh.exchange(pad)
+        # halo rows now hold the neighbours' data exactly
+        np.testing.assert_array_equal(pad.numpy(), u[sh.base:sh.top])
+        got = orc.dss_range(pad.numpy(), side, deg, sh.lo, sh.hi, sh.base, mask=True)
+        want = orc.dss(u, side, deg, mask=True)[sh.lo:sh.hi]
+        np.testing.assert_allclose(got, want, rtol=0, atol=1e-14)
+        dist.barrier()
+        if rank == 0:
+            np.save(result_path, np.array([1.0]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_assembled_halo_exchange_gloo(world, tmp_path):
+    """Multi-GPU assembled CG host logic: each rank's halo (side^2 + side + 1
+    elements either side, from its direct neighbours) holds every copy of
+    every node of its own elements, so the rank-local gather-scatter equals
+    the global one on the rank's range."""
+    res = str(tmp_path / "ok.npy")
+    mp.spawn(_halo_worker, args=(world, _free_port(), res), nprocs=world, join=True)
+    assert np.load(res)[0] == 1.0
+
+
+def test_assembled_shard_ranges():
+    from paper_1711_00903_b200.cg import AssembledShard
+
+    side = 8
+    for world in (1, 2, 4):
+        shards = [AssembledShard(side, 3, r, world) for r in range(world)]
+        assert shards[0].lo == 0 and shards[-1].hi == side ** 3
+        for a, b in zip(shards, shards[1:]):
+            assert a.hi == b.lo
+            assert a.top - a.hi == min(a.halo, side ** 3 - a.hi)
+    with pytest.raises(ValueError):
+        AssembledShard(4, 3, 0, 8)   # 8 elements per rank < 4^2 + 4 + 1
