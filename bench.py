@@ -509,10 +509,7 @@ def run_ours(args):
             "dtype": "f64",
             "data": "synthetic: perturb_mesh(build_cube_mesh(32, 2.0), 0.15, seed=7+rank), "
                     "q = FieldVector.random(seed=0), device-generated geometric factors",
-            "config": {"workload": f"{bp} N={DEGREE} E={mesh.n_el} per GPU (BASELINE configs[1])",
-                       "bp": bp, "degree": DEGREE, "n_el_per_gpu": mesh.n_el, "lam": LAM,
-                       "l2": "inputs larger than L2 (1.21 GB per apply)",
-                       "parallelism": f"element partition x{world}, no data-path collective"},
+            "config": arm_config(bp, mesh.n_el, world),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak,
                          "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": traffic,
                          "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)"
@@ -541,7 +538,18 @@ def run_ours(args):
 # reference arm: the oracle port on the host cores
 # ---------------------------------------------------------------------------
 
+def arm_config(bp, n_el, world):
+    """The `config` both arms report (same workload, same keys)."""
+    return {"workload": f"{bp} N={DEGREE} E={n_el} per GPU (BASELINE configs[1])",
+            "bp": bp, "degree": DEGREE, "n_el_per_gpu": n_el, "lam": LAM,
+            "l2": "inputs larger than L2 (1.21 GB per apply)",
+            "parallelism": f"element partition x{world}, no data-path collective"}
+
+
 def run_reference(args):
+    """The reference arm: the reference's own CPU algorithm for the path (the
+    oracle port -- the reference is pure Python/numpy and does not travel to
+    the GPU box) on all host cores, rank 0 only."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -571,26 +579,34 @@ def run_reference(args):
     def step():
         list(pool.map(work, spans))
 
-    for _ in range(args.warmup):
-        step()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        step()
-    el = time.perf_counter() - t0
+    # one BLAS thread per worker thread: `cores` threads in total, no
+    # oversubscription (numpy releases the GIL inside the BLAS calls)
+    import contextlib
+    try:
+        from threadpoolctl import threadpool_limits
+        limits = threadpool_limits(1)
+    except ImportError:
+        limits = contextlib.nullcontext()
+    with limits:
+        for _ in range(args.warmup):
+            step()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            step()
+        el = time.perf_counter() - t0
     ms = el / args.steps * 1e3
     value = sample * q.shape[1] / (ms * 1e-3) / 1e9
     line = {
-        "metric": METRIC, "value": value, "unit": "GDOF/s", "n_gpus": 0,
+        "metric": METRIC, "value": value, "unit": "GDOF/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "impl": "reference",
         "data": "synthetic: same mesh / q generator as the GPU arm",
-        "config": {"workload": f"{bp} N={DEGREE} E=32768 (BASELINE configs[1]), "
-                               f"bounded sample of {sample} elements per step",
-                   "bp": bp, "degree": DEGREE, "lam": LAM},
+        "config": arm_config(bp, mesh.n_el, 1),
         "cpu_baseline": {"value": value, "unit": "GDOF/s", "cores": cores, "kind": "port",
-                         "sample": f"first {sample} elements, {cores} threads over element "
-                                   "ranges, oracle/hexbench_oracle.py (numpy)"},
+                         "sample": f"bounded sample: first {sample} of the {mesh.n_el} "
+                                   f"elements per step, {cores} threads over element ranges "
+                                   "(1 BLAS thread each), oracle/hexbench_oracle.py (numpy)"},
         "e2e": {"value": value, "unit": "GDOF/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
