@@ -421,6 +421,70 @@ def cg_assembled_report(side=32, iters=20, warmup=3):
             "kernels_per_iteration": 5}
 
 
+def unfused_pass_bytes(bp, deg=DEGREE):
+    """HBM bytes per element of the unfused pass structure (hx_baseline.cu):
+    every pass reads its input tensor and writes its output (the += passes
+    also read the output), pointwise steps read their operands and factors."""
+    n, m = deg + 1, deg + 2
+    interp = (n**3 + n * m * n) + (n * m * n + n * m * m) + (n * m * m + m**3)
+    project = (m**3 + m * n * m) + (m * n * m + m * n * n) + (m * n * n + n**3)
+
+    def chain(p):  # 3 D passes, chain rule (4 in + 7 factors, 4 out), 3 D^T += passes
+        return 6 * p**3 + 15 * p**3 + 9 * p**3
+    doubles = {"BP1.0": interp + 3 * m**3 + project, "BP3.5": chain(n),
+               "BP3.0": interp + chain(m) + project}[bp]
+    return 8 * doubles
+
+
+def baseline_report(steps=5, warmup=2, side=32):
+    """Fused kernels vs the unfused Kernel-1-style path (apply_baseline:
+    one launch per contraction pass, intermediates in HBM -- the paper's
+    reference kernel, and the reference's variant="baseline"
+    access pattern) at N=7, E=32768: the K1 -> fused speed-up on B200.  The
+    baseline's HBM traffic is its pass structure (unfused_pass_bytes); the
+    reference's own baseline counters (perf.element_counters(bp, "baseline",
+    N)) count every term's operand read and are reported beside it."""
+    import torch
+    import paper_1711_00903_b200 as hx
+    from paper_1711_00903_b200.operators import apply_baseline_device, baseline_workspace
+
+    res = {}
+    for bp in hx.BENCHMARKS:
+        mesh, op = build_operator(bp, side, 0)
+        q = hx.FieldVector.random(mesh.n_el, op.n_p, seed=0).to_device().data
+        out = torch.empty_like(q)
+        work = baseline_workspace(op)
+
+        def timed(fn):
+            for _ in range(warmup):
+                fn()
+            torch.cuda.synchronize()
+            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                  for _ in range(steps)]
+            for s, e in ev:
+                s.record()
+                fn()
+                e.record()
+            torch.cuda.synchronize()
+            return statistics.median(s.elapsed_time(e) for s, e in ev)
+
+        t_base = timed(lambda: apply_baseline_device(op, q, out, work))
+        t_fused = timed(lambda: hx.apply_device(op, q, out))
+        c = hx.element_counters(bp, "baseline", DEGREE)
+        counted = (c["global_reads"] + c["global_writes"]) * mesh.n_el
+        passes = unfused_pass_bytes(bp) * mesh.n_el
+        res[bp] = {"n_el": mesh.n_el, "baseline_ms": t_base, "fused_ms": t_fused,
+                   "speedup_fused_over_baseline": t_base / t_fused,
+                   "baseline_gdof_per_s": mesh.n_el * op.n_p / (t_base * 1e-3) / 1e9,
+                   "baseline_pass_bytes": passes,
+                   "baseline_achieved_gb_per_s": passes / (t_base * 1e-3) / 1e9,
+                   "reference_baseline_counted_global_bytes": counted,
+                   "baseline_launches": {"BP1.0": 7, "BP3.5": 7, "BP3.0": 13}[bp]}
+        del op, q, out, work
+        torch.cuda.empty_cache()
+    return res
+
+
 def run_ours(args):
     import torch
     import paper_1711_00903_b200 as hx
@@ -471,6 +535,7 @@ def run_ours(args):
         e2e["frac_of_pcie_bound"] = pcie["bidirectional_ms"] / e2e_ms
     cg = cg_report(op, mesh) if (rank == 0 and not args.quick) else None
     cg_asm = cg_assembled_report() if (rank == 0 and not args.quick) else None
+    unfused = baseline_report() if (rank == 0 and not args.quick) else None
     calib = None
     if rank == 0 and not args.quick:
         import ctypes
@@ -524,6 +589,7 @@ def run_ours(args):
             "per_bp": per_bp,
             "cg": cg,
             "cg_assembled": cg_asm,
+            "unfused_baseline": unfused,
             "calibration": calib,
             "gflop_per_s": hx.flop_model(bp, "fused", DEGREE) * dofs_all / (DEGREE + 1) ** 3
                            / (ms_per_step * 1e-3) / 1e9,

@@ -95,6 +95,16 @@ int hx_apply_host(const hx_plan* plan, const double* q_host, const double* facto
                   double* out_host, int64_t n_el, int64_t chunk_el, void* work,
                   int* status_flag, void* stream);
 
+/* Unfused "baseline" apply: the paper's Kernel-1 structure and
+ * the reference's variant="baseline" access pattern (operators.py:170-200):
+ * one launch per 1-D contraction pass / pointwise step, intermediates in HBM,
+ * in the reference's pass order (operators.py:208-268).  Same result as
+ * hx_apply up to rounding; exists to measure the fused kernels against.
+ * `work` is a device buffer of hx_apply_baseline_workspace(plan, n_el) bytes. */
+int64_t hx_apply_baseline_workspace(const hx_plan* plan, int64_t n_el);
+int hx_apply_baseline(const hx_plan* plan, const double* q, const double* factors, double* out,
+                      int64_t n_el, void* work, int* status_flag, void* stream);
+
 /* Element helpers, batched: replace interpolate_to_gl / project_to_gll
  * (operators.py:352-364), which act on one (n,n,n) / (m,m,m) element tensor.
  * `interp` is the HOST m x n row-major GLL->GL matrix (reference_ops.py:39-44,

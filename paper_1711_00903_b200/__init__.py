@@ -11,7 +11,7 @@ from .mesh import (FACTOR_NAMES, DegenerateGeometryError, GeometricFactors, HexM
                    build_cube_mesh, geometric_factors, perturb_mesh, trilinear_jacobian,
                    trilinear_map)
 from .operators import (AccessCounters, FieldVector, OperatorInstance, UnsupportedVariantError,
-                        apply_bp1, apply_bp3, apply_bp35, apply_device, apply_host,
+                        apply_baseline, apply_bp1, apply_bp3, apply_bp35, apply_device, apply_host,
                         apply_operator, interpolate_to_gl, make_operator,
                         project_to_gll)
 from .perf import (BENCHMARKS, BP1, BP3, BP35, VARIANTS, RooflinePoint, RooflineSeries,

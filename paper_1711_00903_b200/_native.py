@@ -36,6 +36,8 @@ SIGNATURES = {
     "hx_plan_kernel_shape": (_c.c_int, [_P, _c.POINTER(_c.c_int), _c.POINTER(_c.c_int),
                                         _c.POINTER(_c.c_int)]),
     "hx_measure_smem_bandwidth": (_c.c_int, [_c.POINTER(_c.c_double), _P]),
+    "hx_apply_baseline_workspace": (_c.c_int64, [_P, _c.c_int64]),
+    "hx_apply_baseline": (_c.c_int, [_P, _P, _P, _P, _c.c_int64, _P, _P, _P]),
     "hx_interp_elements": (_c.c_int, [_c.c_int, _P, _c.c_int, _P, _P, _c.c_int64, _P, _P]),
     "hx_energy_partials": (_c.c_int64, []),
     "hx_apply_energy": (_c.c_int, [_P, _P, _P, _P, _c.c_int64, _P, _c.c_int64, _P, _P, _P]),

@@ -175,6 +175,22 @@ int hx_apply(const hx_plan* P, const double* q, const double* factors, double* o
   return cuda_status(launch(*P, q, factors, out, n_el, flag, static_cast<cudaStream_t>(stream)));
 }
 
+int64_t hx_apply_baseline_workspace(const hx_plan* P, int64_t n_el) {
+  if (!P || n_el < 0) return -1;
+  return baseline_workspace_doubles(*P, n_el) * int64_t(sizeof(double));
+}
+
+int hx_apply_baseline(const hx_plan* P, const double* q, const double* factors, double* out,
+                      int64_t n_el, void* work, int* flag, void* stream) {
+  if (!P || n_el < 0) return HX_EINVAL;
+  if (n_el > 0 && (!q || !factors || !out || !work)) return HX_EINVAL;
+  if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(factors) |
+       reinterpret_cast<uintptr_t>(out) | reinterpret_cast<uintptr_t>(work)) & 7)
+    return HX_EINVAL;
+  return cuda_status(launch_baseline(*P, q, factors, out, n_el, static_cast<double*>(work), flag,
+                                     static_cast<cudaStream_t>(stream)));
+}
+
 int hx_interp_elements(int degree, const double* interp, int project, const double* src,
                        double* dst, int64_t n_el, int* flag, void* stream) {
   if (degree < 1 || degree > 15 || n_el < 0 || !interp) return HX_EINVAL;

@@ -40,6 +40,9 @@ cudaError_t launch_bp35(const hx_plan& P, const double* q, const double* fac, do
                         int64_t n_el, int* flag, double* energy, cudaStream_t s);
 cudaError_t launch_bp3(const hx_plan& P, const double* q, const double* fac, double* out,
                        int64_t n_el, int* flag, double* energy, cudaStream_t s);
+cudaError_t launch_baseline(const hx_plan& P, const double* q, const double* fac, double* out,
+                            int64_t n_el, double* work, int* flag, cudaStream_t s);
+int64_t baseline_workspace_doubles(const hx_plan& P, int64_t n_el);
 cudaError_t launch_interp(int degree, const double* interp, int project, const double* src,
                           double* dst, int64_t n_el, int* flag, cudaStream_t s);
 cudaError_t launch_geometry(const hx_plan& P, const double* verts, int64_t n_el, int all_slots,

@@ -307,6 +307,43 @@ def apply_host(op, src, dst, flag=None, stream=None, chunk_el=None, work=None):
     return _apply_host(op, src, dst, flag, stream, chunk_el, work)
 
 
+def baseline_workspace(op):
+    """Device scratch for apply_baseline (4 GL-point tensors per element)."""
+    import torch
+
+    nbytes = _native.lib().hx_apply_baseline_workspace(op.plan.handle, op.n_el)
+    return torch.empty(max(1, nbytes // DOUBLE), dtype=torch.float64, device=op.device)
+
+
+def apply_baseline_device(op, q, out, work, flag=None, stream=None):
+    """Raw unfused apply (asynchronous, no allocation, no sync): see
+    apply_baseline."""
+    if stream is None:
+        stream = _stream(op.device)
+    _native.check(_native.lib().hx_apply_baseline(
+        op.plan.handle, _native.ptr(q), _native.ptr(op.device_factors), _native.ptr(out),
+        op.n_el, _native.ptr(work), _native.ptr(flag), stream), "hx_apply_baseline")
+
+
+def apply_baseline(op, q, out=None, stream=None):
+    """Unfused apply on device tensors: the paper's Kernel-1 structure
+     -- one launch per contraction pass, intermediates through
+    HBM, the pass order of operators.py:208-268 -- i.e. what the reference's
+    ``variant="baseline"`` counters describe.  Same result as the fused
+    kernels up to rounding; exists so the fused kernels can be measured
+    against it (bench.py).  ``q``: (n_el, n_p) float64 CUDA tensor."""
+    import torch
+
+    if tuple(q.shape) != (op.n_el, op.n_p):
+        raise ValueError("field vector shape does not match operator")
+    out = torch.empty_like(q) if out is None else out
+    flag = torch.zeros(1, dtype=torch.int32, device=q.device)
+    apply_baseline_device(op, q, out, baseline_workspace(op), flag, stream)
+    if int(flag.item()) & _native.HX_FLAG_NONFINITE:
+        raise ValueError("field vector contains non-finite values")
+    return out
+
+
 def apply_bp1(op, q, counters=None, threads=1):
     if op.bp != BP1:
         raise ValueError("operator is not BP1.0")

@@ -257,3 +257,24 @@ def test_full_size_config_sampled_parity_and_symmetry(bp):
     w = hx.FieldVector(mesh.n_el, op.n_p, 2 * u.data - v.data)
     aw = hx.apply_operator(op, w).data
     assert float((aw - (2 * au - av)).norm() / aw.norm()) <= 1e-14
+
+
+@pytest.mark.parametrize("bp", BPS)
+@pytest.mark.parametrize("deg", [1, 2, 4, 7, 8, 15])
+def test_unfused_baseline_path_matches_oracle(bp, deg, mesh3):
+    """apply_baseline (paper Kernel-1 structure, intermediates in HBM) gives
+    the same operator as the fused kernels and the oracle."""
+    rng = np.random.default_rng(100 + deg)
+    for n_el in (1, 27):
+        op = hx.make_operator(bp, deg, sub_mesh(mesh3, n_el), lam=0.7)
+        q = rng.standard_normal((n_el, op.n_p))
+        got = hx.apply_baseline(op, torch.from_numpy(q).cuda()).cpu().numpy()
+        ref = oracle_apply(op, q)
+        assert orc.rel_l2(got, ref) <= PARITY, (bp, deg, n_el, orc.rel_l2(got, ref))
+        np.testing.assert_allclose(got, dev_apply(op, q), rtol=0,
+                                   atol=1e-12 * max(1.0, np.abs(ref).max()))
+    bad = torch.zeros((1, op.n_p), dtype=torch.float64, device="cuda")
+    bad[0, 0] = float("inf")
+    op1 = hx.make_operator(bp, deg, sub_mesh(mesh3, 1), lam=0.7)
+    with pytest.raises(ValueError):
+        hx.apply_baseline(op1, bad)
