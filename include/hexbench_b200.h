@@ -168,6 +168,22 @@ int hx_cg_update_dss(double* x, const double* p, double* r, const double* ap, in
                      int64_t ap_base, const double* rr, const double* pap, double* partials,
                      int64_t n_partials, double* rr_new, void* stream);
 
+/* Separable in-place gather-scatter: u (a buffer holding elements
+ * [buf_begin, buf_end)) <- Q Q^T u as three per-axis face passes (each copy of
+ * a face node becomes lower-element copy + upper-element copy).  Exact for
+ * every node whose copies all lie in the buffer (a rank's own elements, given
+ * its halo); bitwise deterministic and continuous, but summed in pass order,
+ * not hx_dss's gather order.  No masking.
+ *   hx_cg_update_masked: hx_cg_update with r -= alpha mask w for an already
+ *   assembled w (elements from w_base on) and the multiplicity-weighted
+ *   <r, r> -- the per-iteration update of the assembled CG.              */
+int hx_dss_inplace(double* u, int side, int degree, int64_t buf_begin, int64_t buf_end,
+                   void* stream);
+int hx_cg_update_masked(double* x, const double* p, double* r, const double* w, int side,
+                        int degree, int mask_boundary, int64_t e_begin, int64_t e_end,
+                        int64_t w_base, const double* rr, const double* pap, double* partials,
+                        int64_t n_partials, double* rr_new, void* stream);
+
 /* Elements each CTA processes per tile, threads per CTA and dynamic shared
  * memory bytes of the plan's kernel (for reports and tests).                */
 int hx_plan_kernel_shape(const hx_plan* plan, int* elements_per_tile, int* threads,

@@ -222,3 +222,21 @@ def dss_range(pad, side, degree, e_begin, e_end, base, mask=False):
     if mask:
         s[cube_boundary(side, degree)] = 0.0
     return s[gidx[e_begin:e_end]]
+
+
+def dss_passes(u, side, degree):
+    """Q Q^T as three per-axis face passes (csrc/hx_dss.cu dss_pass_kernel):
+    for every interior face normal to x, then y, then z, both copies of each
+    face node become (lower-element copy + upper-element copy)."""
+    n, N = degree + 1, degree
+    t = np.array(u, dtype=np.float64).reshape(side, side, side, n, n, n)  # cx,cy,cz,k,j,i
+    # x: element axis 0, local i (axis 5); y: axis 1, local j (axis 4); z: axis 2, k (axis 3)
+    for eax, lax in ((0, 5), (1, 4), (2, 3)):
+        lo = [slice(None)] * 6
+        hi = [slice(None)] * 6
+        lo[eax], lo[lax] = slice(0, side - 1), N       # lower element's upper face
+        hi[eax], hi[lax] = slice(1, side), 0           # upper element's lower face
+        s = t[tuple(lo)] + t[tuple(hi)]
+        t[tuple(lo)] = s
+        t[tuple(hi)] = s
+    return t.reshape(np.shape(u))

@@ -267,7 +267,9 @@ def _assembled_setup(op, side, b, st, stream):
 
 
 def _assembled_step(op, side, st, cur, stream, flag=None):
-    """One CG iteration; returns the index of the new <r, r> slot."""
+    """One CG iteration; returns the index of the new <r, r> slot.  A p is
+    assembled in place by the separable face passes (hx_dss_inplace) over
+    the halo-padded buffer, then read plainly by the update."""
     L, ptr, sh, w = _native.lib(), _native.ptr, st.sh, st.w
     nxt = 1 - cur
     ap_own = sh.own(st.ap_pad)
@@ -276,10 +278,12 @@ def _assembled_step(op, side, st, cur, stream, flag=None):
                                     ptr(flag), stream), "hx_apply_energy")
     _global_sum(w.pap, sh)
     sh.exchange(st.ap_pad)
-    _native.check(L.hx_cg_update_dss(ptr(st.x), ptr(w.p), ptr(w.r), ptr(st.ap_pad), side,
-                                     op.degree, st.mask, sh.lo, sh.hi, sh.base, ptr(w.rr[cur]),
-                                     ptr(w.pap), ptr(w.partials), w.npart, ptr(w.rr[nxt]),
-                                     stream), "hx_cg_update_dss")
+    _native.check(L.hx_dss_inplace(ptr(st.ap_pad), side, op.degree, sh.base, sh.top, stream),
+                  "hx_dss_inplace")
+    _native.check(L.hx_cg_update_masked(ptr(st.x), ptr(w.p), ptr(w.r), ptr(st.ap_pad), side,
+                                        op.degree, st.mask, sh.lo, sh.hi, sh.base,
+                                        ptr(w.rr[cur]), ptr(w.pap), ptr(w.partials), w.npart,
+                                        ptr(w.rr[nxt]), stream), "hx_cg_update_masked")
     _global_sum(w.rr[nxt], sh)
     return nxt
 
@@ -296,9 +300,10 @@ def cg_solve_assembled(op, side, b, tol=1e-10, maxiter=1000, check_every=10,
     conditions when ``mask_boundary`` (needed for BP3.5 / BP3.0 with
     lam = 0).  Returns a CGResult whose ``x`` is continuous (every copy of a
     global node holds the same value).  Per iteration: the fused matvec +
-    <p, A p>, the halo exchange (multi-GPU), one update kernel that gathers
-    A p across element copies on the fly (the assembled vector is never
-    stored), the direction update.
+    <p, A p>, the halo exchange (multi-GPU), the gather-scatter of
+    A p in place with three per-axis face passes, the update (plain read of
+    the assembled A p, masked, multiplicity-weighted <r, r>), the direction
+    update.
     """
     import torch
 

@@ -354,6 +354,28 @@ int hx_cg_update_dss(double* x, const double* p, double* r, const double* ap, in
                                           static_cast<cudaStream_t>(stream)));
 }
 
+int hx_dss_inplace(double* u, int side, int degree, int64_t buf_begin, int64_t buf_end,
+                   void* stream) {
+  if (!dss_args_ok(side, degree, buf_begin, buf_end)) return HX_EINVAL;
+  if (buf_end > buf_begin && !u) return HX_EINVAL;
+  return cuda_status(launch_dss_inplace(u, side, degree, buf_begin, buf_end,
+                                        static_cast<cudaStream_t>(stream)));
+}
+
+int hx_cg_update_masked(double* x, const double* p, double* r, const double* w, int side,
+                        int degree, int mask, int64_t e_begin, int64_t e_end, int64_t w_base,
+                        const double* rr, const double* pap, double* partials,
+                        int64_t n_partials, double* rr_new, void* stream) {
+  if (!dss_args_ok(side, degree, e_begin, e_end) || w_base < 0 || w_base > e_begin)
+    return HX_EINVAL;
+  if (!rr || !pap || !partials || !rr_new) return HX_EINVAL;
+  if (e_end > e_begin && (!x || !p || !r || !w)) return HX_EINVAL;
+  if (n_partials < hx_energy_partials()) return HX_EINVAL;
+  return cuda_status(launch_cg_update_masked(x, p, r, w, side, degree, mask != 0, e_begin,
+                                             e_end, w_base, rr, pap, partials, rr_new,
+                                             static_cast<cudaStream_t>(stream)));
+}
+
 int hx_measure_smem_bandwidth(double* bytes_per_s, void* stream) {
   if (!bytes_per_s) return HX_EINVAL;
   cudaStream_t s = static_cast<cudaStream_t>(stream);

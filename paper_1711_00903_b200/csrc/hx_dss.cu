@@ -179,6 +179,76 @@ __global__ void __launch_bounds__(kDssThreads)
   if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
+// ---- separable in-place gather-scatter ------------------------------------
+// Q Q^T on the cube mesh is a Kronecker product of 1-D gather-scatters, so it
+// can be applied as three passes, one per axis: each pass replaces both
+// copies of every node on an interior element face normal to that axis by
+// (lower-element copy + upper-element copy).  After the x, y and z passes
+// every copy of a node holds the same bits (addition is commutative and the
+// operands of each pair are the same on both sides), and each pass only
+// touches face nodes -- far cheaper than gathering up to 8 copies per node.
+// A buffer holding elements [lo, hi) gets the correct result for every node
+// whose copies all lie in the buffer (a rank's own nodes, given its halo).
+template <int N, int AX>
+__global__ void __launch_bounds__(kDssThreads)
+    dss_pass_kernel(double* __restrict__ u, int side, int64_t lo, int64_t hi) {
+  constexpr int n = N + 1, n2 = n * n, n3 = n2 * n;
+  const int64_t s = side;
+  const int64_t estride = AX == 0 ? s * s : (AX == 1 ? s : 1);  // x: cx, y: cy, z: cz
+  const int64_t total = (hi - lo) * n2;
+  for (int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; g < total;
+       g += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t e = lo + g / n2;
+    const int f = int(g % n2);
+    const int c = AX == 0 ? int(e / (s * s)) : (AX == 1 ? int((e / s) % s) : int(e % s));
+    const int64_t nb = e - estride;  // lower neighbour along the axis
+    if (c == 0 || nb < lo) continue;
+    // face node f of the element's lower face (local index 0 along AX) and
+    // the matching node on the neighbour's upper face (local index N)
+    int lo_off, hi_off;
+    if constexpr (AX == 0) {          // i = 0 / N, f = (k, j)
+      lo_off = f * n;                 // (k * n + j) * n + 0
+      hi_off = f * n + N;
+    } else if constexpr (AX == 1) {   // j = 0 / N, f = (k, i)
+      const int k = f / n, i = f % n;
+      lo_off = k * n2 + i;
+      hi_off = k * n2 + N * n + i;
+    } else {                          // k = 0 / N, f = (j, i)
+      lo_off = f;
+      hi_off = N * n2 + f;
+    }
+    double* a = u + (nb - lo) * n3 + hi_off;  // lower element's copy
+    double* b = u + (e - lo) * n3 + lo_off;   // upper element's copy
+    const double sum = *a + *b;
+    *a = sum;
+    *b = sum;
+  }
+}
+
+// alpha = rr / pAp;  x += alpha p;  r -= alpha mask w (w already assembled);
+// partials of sum r^2 / multiplicity
+template <int N>
+__global__ void __launch_bounds__(kDssThreads)
+    cg_update_masked_kernel(double* __restrict__ x, const double* __restrict__ p,
+                            double* __restrict__ r, const double* __restrict__ w, DssRange g,
+                            int mask, const double* __restrict__ rr,
+                            const double* __restrict__ pap, double* __restrict__ part) {
+  constexpr int n3 = (N + 1) * (N + 1) * (N + 1);
+  __shared__ double scratch[kDssThreads / 32];
+  const double alpha = rr[0] / pap[0];
+  const int64_t woff = (g.e_begin - g.base) * n3;
+  double s = 0.0;
+  for_nodes<N>(g, [&](const NodeRef& nr, int64_t idx) {
+    const double wv = (mask && on_boundary<N>(nr, g.side)) ? 0.0 : w[woff + idx];
+    x[idx] = fma(alpha, p[idx], x[idx]);
+    const double ri = fma(-alpha, wv, r[idx]);
+    r[idx] = ri;
+    s = fma(ri, ri * inv_mult<N>(nr, g.side), s);
+  });
+  s = block_sum<kDssThreads>(s, scratch);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
 static int dss_blocks(const DssRange& g) {
   const int64_t n_el = g.e_end - g.e_begin;
   const int64_t cap = int64_t(sm_count()) * 8;
@@ -239,6 +309,40 @@ cudaError_t launch_cg_update_dss(double* x, const double* p, double* r, const do
 #define HX_CALL(N)                                                                            \
   cg_update_dss_kernel<N><<<nb, kDssThreads, 0, s>>>(x, p, r, ap, g, mask, rr, pap, part);   \
   if ((err = cudaGetLastError()) != cudaSuccess) return err;                                 \
+  return launch_sum(part, nb, rr_new, s);
+  HX_DSS_DISPATCH(HX_CALL)
+#undef HX_CALL
+}
+
+cudaError_t launch_dss_inplace(double* u, int side, int degree, int64_t lo, int64_t hi,
+                               cudaStream_t s) {
+  if (hi <= lo) return cudaSuccess;
+  const int64_t work = (hi - lo) * int64_t(degree + 1) * (degree + 1);
+  const int64_t want = (work + kDssThreads - 1) / kDssThreads;
+  const int nb = int(want < int64_t(sm_count()) * 16 ? want : int64_t(sm_count()) * 16);
+  cudaError_t err;
+#define HX_CALL(N)                                                                \
+  dss_pass_kernel<N, 0><<<nb, kDssThreads, 0, s>>>(u, side, lo, hi);             \
+  if ((err = cudaGetLastError()) != cudaSuccess) return err;                     \
+  dss_pass_kernel<N, 1><<<nb, kDssThreads, 0, s>>>(u, side, lo, hi);             \
+  if ((err = cudaGetLastError()) != cudaSuccess) return err;                     \
+  dss_pass_kernel<N, 2><<<nb, kDssThreads, 0, s>>>(u, side, lo, hi);             \
+  return cudaGetLastError();
+  HX_DSS_DISPATCH(HX_CALL)
+#undef HX_CALL
+}
+
+cudaError_t launch_cg_update_masked(double* x, const double* p, double* r, const double* w,
+                                    int side, int degree, int mask, int64_t e_begin,
+                                    int64_t e_end, int64_t w_base, const double* rr,
+                                    const double* pap, double* part, double* rr_new,
+                                    cudaStream_t s) {
+  const DssRange g = range(side, e_begin, e_end, w_base);
+  const int nb = dss_blocks(g);
+  cudaError_t err;
+#define HX_CALL(N)                                                                           \
+  cg_update_masked_kernel<N><<<nb, kDssThreads, 0, s>>>(x, p, r, w, g, mask, rr, pap, part); \
+  if ((err = cudaGetLastError()) != cudaSuccess) return err;                                \
   return launch_sum(part, nb, rr_new, s);
   HX_DSS_DISPATCH(HX_CALL)
 #undef HX_CALL

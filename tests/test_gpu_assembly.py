@@ -145,6 +145,29 @@ def test_dss_range_semantics_match_global(world):
     assert abs(total - ref) <= 1e-12 * ref
 
 
+@pytest.mark.parametrize("side,deg", [(1, 2), (3, 3), (4, 7)])
+def test_inplace_separable_dss_matches_oracle(side, deg):
+    """hx_dss_inplace (three face passes) == the oracle's pass form bit for
+    bit, == Q Q^T to rounding; a rank's halo-padded buffer reproduces the
+    full result on its own elements exactly."""
+    from paper_1711_00903_b200.cg import AssembledShard
+
+    n3 = (deg + 1) ** 3
+    u = np.random.default_rng(side * 7 + deg).standard_normal((side ** 3, n3))
+    L = _native.lib()
+    ud = torch.from_numpy(u).cuda()
+    _native.check(L.hx_dss_inplace(_native.ptr(ud), side, deg, 0, side ** 3, None))
+    got = ud.cpu().numpy()
+    np.testing.assert_array_equal(got, orc.dss_passes(u, side, deg))
+    assert orc.rel_l2(got, orc.dss(u, side, deg)) <= 1e-15
+    if side ** 3 >= 2 * (side * side + side + 1):
+        for r in range(2):
+            sh = AssembledShard(side, deg, r, 2)
+            pad = torch.from_numpy(u[sh.base:sh.top].copy()).cuda()
+            _native.check(L.hx_dss_inplace(_native.ptr(pad), side, deg, sh.base, sh.top, None))
+            np.testing.assert_array_equal(sh.own(pad).cpu().numpy(), got[sh.lo:sh.hi])
+
+
 def test_dss_argument_errors():
     u = torch.zeros(8 * 27, dtype=torch.float64, device="cuda")
     with pytest.raises(ValueError):
