@@ -145,7 +145,7 @@ int hx_cg_direction(double* p, const double* r, int64_t n, const double* rr_new,
  * (mesh.py:44-56; element e = (cx*side + cy)*side + cz, local (k,j,i) is
  * global node (cx N + i, cy N + j, cz N + k)).  New: the reference has no
  * assembly; this serves the assembled CG solve.
- * Each call processes the elements [e_begin, e_end) (a rank's shard; 0 and
+ * side <= 1600.  Each call processes the elements [e_begin, e_end) (a rank's shard; 0 and
  * side^3 on one GPU).  Own vectors (out, u, v, x, p, r) hold exactly those
  * elements; the GATHERED vector (in, ap) holds elements from `*_base` on and
  * must include every element that shares a node with the range (at most

@@ -316,7 +316,8 @@ int hx_cg_direction(double* p, const double* r, int64_t n, const double* rr_new,
 }
 
 static bool dss_args_ok(int side, int degree, int64_t e_begin, int64_t e_end) {
-  return side >= 1 && side <= 4096 && degree >= 1 && degree <= 15 && e_begin >= 0 &&
+  // side <= 1600 keeps element indices below 2^32 (32-bit index math)
+  return side >= 1 && side <= 1600 && degree >= 1 && degree <= 15 && e_begin >= 0 &&
          e_begin <= e_end && e_end <= int64_t(side) * side * side;
 }
 
