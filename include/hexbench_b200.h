@@ -174,15 +174,17 @@ int hx_cg_update_dss(double* x, const double* p, double* r, const double* ap, in
  * every node whose copies all lie in the buffer (a rank's own elements, given
  * its halo); bitwise deterministic and continuous, but summed in pass order,
  * not hx_dss's gather order.  No masking.
- *   hx_cg_update_masked: hx_cg_update with r -= alpha mask w for an already
- *   assembled w (elements from w_base on) and the multiplicity-weighted
- *   <r, r> -- the per-iteration update of the assembled CG.              */
+ *   hx_cg_update_assembled: the assembled-CG update -- ap (= A_L p for the
+ *   elements [ap_base, ap_end): own range plus exchanged halo; used as
+ *   scratch and overwritten) is assembled in place (the three face passes),
+ *   then as hx_cg_update with
+ *   r -= alpha mask (Q Q^T ap) and the multiplicity-weighted <r, r>.     */
 int hx_dss_inplace(double* u, int side, int degree, int64_t buf_begin, int64_t buf_end,
                    void* stream);
-int hx_cg_update_masked(double* x, const double* p, double* r, const double* w, int side,
-                        int degree, int mask_boundary, int64_t e_begin, int64_t e_end,
-                        int64_t w_base, const double* rr, const double* pap, double* partials,
-                        int64_t n_partials, double* rr_new, void* stream);
+int hx_cg_update_assembled(double* x, const double* p, double* r, double* ap, int side,
+                           int degree, int mask_boundary, int64_t e_begin, int64_t e_end,
+                           int64_t ap_base, int64_t ap_end, const double* rr, const double* pap,
+                           double* partials, int64_t n_partials, double* rr_new, void* stream);
 
 /* Elements each CTA processes per tile, threads per CTA and dynamic shared
  * memory bytes of the plan's kernel (for reports and tests).                */

@@ -51,9 +51,9 @@ SIGNATURES = {
     "hx_cg_update_dss": (_c.c_int, [_P, _P, _P, _P, _c.c_int, _c.c_int, _c.c_int, _c.c_int64,
                                     _c.c_int64, _c.c_int64, _P, _P, _P, _c.c_int64, _P, _P]),
     "hx_dss_inplace": (_c.c_int, [_P, _c.c_int, _c.c_int, _c.c_int64, _c.c_int64, _P]),
-    "hx_cg_update_masked": (_c.c_int, [_P, _P, _P, _P, _c.c_int, _c.c_int, _c.c_int,
-                                       _c.c_int64, _c.c_int64, _c.c_int64, _P, _P, _P,
-                                       _c.c_int64, _P, _P]),
+    "hx_cg_update_assembled": (_c.c_int, [_P, _P, _P, _P, _c.c_int, _c.c_int, _c.c_int,
+                                          _c.c_int64, _c.c_int64, _c.c_int64, _c.c_int64,
+                                          _P, _P, _P, _c.c_int64, _P, _P]),
     "hx_strerror": (_c.c_char_p, [_c.c_int]),
     "hx_device_ok": (_c.c_int, []),
 }

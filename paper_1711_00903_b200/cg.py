@@ -268,8 +268,8 @@ def _assembled_setup(op, side, b, st, stream):
 
 def _assembled_step(op, side, st, cur, stream, flag=None):
     """One CG iteration; returns the index of the new <r, r> slot.  A p is
-    assembled in place by the separable face passes (hx_dss_inplace) over
-    the halo-padded buffer, then read plainly by the update."""
+    assembled in place over the halo-padded buffer by the separable face
+    passes, then read by the masked update (hx_cg_update_assembled)."""
     L, ptr, sh, w = _native.lib(), _native.ptr, st.sh, st.w
     nxt = 1 - cur
     ap_own = sh.own(st.ap_pad)
@@ -278,12 +278,10 @@ def _assembled_step(op, side, st, cur, stream, flag=None):
                                     ptr(flag), stream), "hx_apply_energy")
     _global_sum(w.pap, sh)
     sh.exchange(st.ap_pad)
-    _native.check(L.hx_dss_inplace(ptr(st.ap_pad), side, op.degree, sh.base, sh.top, stream),
-                  "hx_dss_inplace")
-    _native.check(L.hx_cg_update_masked(ptr(st.x), ptr(w.p), ptr(w.r), ptr(st.ap_pad), side,
-                                        op.degree, st.mask, sh.lo, sh.hi, sh.base,
-                                        ptr(w.rr[cur]), ptr(w.pap), ptr(w.partials), w.npart,
-                                        ptr(w.rr[nxt]), stream), "hx_cg_update_masked")
+    _native.check(L.hx_cg_update_assembled(ptr(st.x), ptr(w.p), ptr(w.r), ptr(st.ap_pad), side,
+                                           op.degree, st.mask, sh.lo, sh.hi, sh.base, sh.top,
+                                           ptr(w.rr[cur]), ptr(w.pap), ptr(w.partials), w.npart,
+                                           ptr(w.rr[nxt]), stream), "hx_cg_update_assembled")
     _global_sum(w.rr[nxt], sh)
     return nxt
 

@@ -26,6 +26,17 @@
 #define HX_MINB_BP1_OF(N) Cfg<kBP1, N>::MINB
 #endif
 
+// HX_BP1_SHARED_FOLD: apply I^T from I's own fold (fold_apply_T) instead of
+// a second coefficient set, so S3's I_t and I_t^T read the same constants.
+#ifndef HX_BP1_SHARED_FOLD
+#define HX_BP1_SHARED_FOLD 0
+#endif
+#if HX_BP1_SHARED_FOLD
+#define HX_BP1_PROJECT(in, out) fold_apply_T<m, n>(p.I, in, out)
+#else
+#define HX_BP1_PROJECT(in, out) fold_apply<n, m, 1>(p.It, in, out)
+#endif
+
 namespace hx {
 
 template <int N>
@@ -193,7 +204,7 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT, HX_MINB_BP1_OF(N))
         if constexpr (ENERGY) en += wy * y[t];  // <q, A q> = sum GwJ (I q)^2
         y[t] = wy;
       }
-      fold_apply<n, m, 1>(p.It, y, x);
+      HX_BP1_PROJECT(y, x);
 #pragma unroll
       for (int t = 0; t < n; ++t) line[LY.kofs(t)] = x[t];
     });
@@ -208,7 +219,7 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT, HX_MINB_BP1_OF(N))
       double x[m], y[n];
 #pragma unroll
       for (int t = 0; t < m; ++t) x[t] = src[t];
-      fold_apply<n, m, 1>(p.It, x, y);
+      HX_BP1_PROJECT(x, y);
       double* dst = X + el * EX + LX.kofs(k) + a * LX.s1;
 #pragma unroll
       for (int t = 0; t < n; ++t) dst[t] = y[t];
@@ -224,7 +235,7 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT, HX_MINB_BP1_OF(N))
       double x[m], y[n];
 #pragma unroll
       for (int t = 0; t < m; ++t) x[t] = src[t * LX.s1];
-      fold_apply<n, m, 1>(p.It, x, y);
+      HX_BP1_PROJECT(x, y);
       double* dst = p.out + (e0 + el) * n3 + k * n2 + i;
 #pragma unroll
       for (int t = 0; t < n; ++t) st_stream(dst + t * n, y[t]);

@@ -363,18 +363,19 @@ int hx_dss_inplace(double* u, int side, int degree, int64_t buf_begin, int64_t b
                                         static_cast<cudaStream_t>(stream)));
 }
 
-int hx_cg_update_masked(double* x, const double* p, double* r, const double* w, int side,
-                        int degree, int mask, int64_t e_begin, int64_t e_end, int64_t w_base,
-                        const double* rr, const double* pap, double* partials,
-                        int64_t n_partials, double* rr_new, void* stream) {
-  if (!dss_args_ok(side, degree, e_begin, e_end) || w_base < 0 || w_base > e_begin)
+int hx_cg_update_assembled(double* x, const double* p, double* r, double* ap, int side,
+                           int degree, int mask, int64_t e_begin, int64_t e_end, int64_t ap_base,
+                           int64_t ap_end, const double* rr, const double* pap, double* partials,
+                           int64_t n_partials, double* rr_new, void* stream) {
+  if (!dss_args_ok(side, degree, e_begin, e_end) || ap_base < 0 || ap_base > e_begin ||
+      ap_end < e_end || ap_end > int64_t(side) * side * side)
     return HX_EINVAL;
   if (!rr || !pap || !partials || !rr_new) return HX_EINVAL;
-  if (e_end > e_begin && (!x || !p || !r || !w)) return HX_EINVAL;
+  if (e_end > e_begin && (!x || !p || !r || !ap)) return HX_EINVAL;
   if (n_partials < hx_energy_partials()) return HX_EINVAL;
-  return cuda_status(launch_cg_update_masked(x, p, r, w, side, degree, mask != 0, e_begin,
-                                             e_end, w_base, rr, pap, partials, rr_new,
-                                             static_cast<cudaStream_t>(stream)));
+  return cuda_status(launch_cg_update_assembled(x, p, r, ap, side, degree, mask != 0, e_begin,
+                                                e_end, ap_base, ap_end, rr, pap, partials,
+                                                rr_new, static_cast<cudaStream_t>(stream)));
 }
 
 int hx_measure_smem_bandwidth(double* bytes_per_s, void* stream) {

@@ -232,26 +232,67 @@ __global__ void __launch_bounds__(kDssThreads)
   }
 }
 
-// alpha = rr / pAp;  x += alpha p;  r -= alpha mask w (w already assembled);
-// partials of sum r^2 / multiplicity
+// Assembled-CG update.  w (= A_L p, halo-padded, elements from g.base on)
+// has been assembled in place by the three face passes; then
+//   alpha = rr / pAp;  x += alpha p;  r -= alpha mask w;  partials of
+//   sum r^2 / multiplicity.
+// >= 6 CTAs of 256 threads per SM (<= 40 registers, no spills): this kernel
+// lives on memory parallelism (r15 ncu: 60 registers halved the resident
+// warps and made it 1.5x slower than the element-local update).  Folding the
+// strided x pass into it as a neighbour gather measured slower still (r16).
 template <int N>
-__global__ void __launch_bounds__(kDssThreads)
-    cg_update_masked_kernel(double* __restrict__ x, const double* __restrict__ p,
-                            double* __restrict__ r, const double* __restrict__ w, DssRange g,
-                            int mask, const double* __restrict__ rr,
-                            const double* __restrict__ pap, double* __restrict__ part) {
-  constexpr int n3 = (N + 1) * (N + 1) * (N + 1);
+__global__ void __launch_bounds__(kDssThreads, 6)
+    cg_update_assembled_kernel(double* __restrict__ x, const double* __restrict__ p,
+                               double* __restrict__ r, const double* __restrict__ w, DssRange g,
+                               int mask, const double* __restrict__ rr,
+                               const double* __restrict__ pap, double* __restrict__ part) {
+  // written out instead of through for_nodes: inside the lambda the
+  // compiler lost __restrict__ and serialised each node's loads behind the
+  // previous node's stores (r17: 179 us vs 118 us for the plain update)
+  constexpr int n = N + 1, n3 = n * n * n;
+  constexpr int IT = (n3 + kDssThreads - 1) / kDssThreads;
+  constexpr int CH = IT < 2 ? IT : 2;  // nodes per thread with loads in flight together
   __shared__ double scratch[kDssThreads / 32];
   const double alpha = rr[0] / pap[0];
-  const int64_t woff = (g.e_begin - g.base) * n3;
+  const double* __restrict__ wown = w + (g.e_begin - g.base) * n3;
+  const uint32_t s32 = uint32_t(g.side);
   double s = 0.0;
-  for_nodes<N>(g, [&](const NodeRef& nr, int64_t idx) {
-    const double wv = (mask && on_boundary<N>(nr, g.side)) ? 0.0 : w[woff + idx];
-    x[idx] = fma(alpha, p[idx], x[idx]);
-    const double ri = fma(-alpha, wv, r[idx]);
-    r[idx] = ri;
-    s = fma(ri, ri * inv_mult<N>(nr, g.side), s);
-  });
+  for (int64_t e = g.e_begin + blockIdx.x; e < g.e_end; e += gridDim.x) {
+    const uint32_t e32 = uint32_t(e), exy = e32 / s32;
+    NodeRef nr;
+    nr.e = e;
+    nr.cz = int(e32 - exy * s32);
+    nr.cx = int(exy / s32);
+    nr.cy = int(exy - uint32_t(nr.cx) * s32);
+    const int64_t own = (e - g.e_begin) * n3;
+    for (int i0 = 0; i0 < IT; i0 += CH) {
+      double pv[CH], xv[CH], rv[CH], wv[CH];
+#pragma unroll
+      for (int c = 0; c < CH; ++c) {  // the chunk's loads first
+        const int l = threadIdx.x + (i0 + c) * kDssThreads;
+        if (l < n3) {
+          pv[c] = p[own + l];
+          xv[c] = x[own + l];
+          rv[c] = r[own + l];
+          wv[c] = wown[own + l];
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < CH; ++c) {
+        const int l = threadIdx.x + (i0 + c) * kDssThreads;
+        if (l < n3) {
+          nr.i = l % n;
+          nr.j = (l / n) % n;
+          nr.k = l / (n * n);
+          const double wm = (mask && on_boundary<N>(nr, g.side)) ? 0.0 : wv[c];
+          x[own + l] = fma(alpha, pv[c], xv[c]);
+          const double ri = fma(-alpha, wm, rv[c]);
+          r[own + l] = ri;
+          s = fma(ri, ri * inv_mult<N>(nr, g.side), s);
+        }
+      }
+    }
+  }
   s = block_sum<kDssThreads>(s, scratch);
   if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
@@ -339,16 +380,27 @@ cudaError_t launch_dss_inplace(double* u, int side, int degree, int64_t lo, int6
 #undef HX_CALL
 }
 
-cudaError_t launch_cg_update_masked(double* x, const double* p, double* r, const double* w,
-                                    int side, int degree, int mask, int64_t e_begin,
-                                    int64_t e_end, int64_t w_base, const double* rr,
-                                    const double* pap, double* part, double* rr_new,
-                                    cudaStream_t s) {
-  const DssRange g = range(side, e_begin, e_end, w_base);
+cudaError_t launch_cg_update_assembled(double* x, const double* p, double* r, double* ap,
+                                       int side, int degree, int mask, int64_t e_begin,
+                                       int64_t e_end, int64_t ap_base, int64_t ap_end,
+                                       const double* rr, const double* pap, double* part,
+                                       double* rr_new, cudaStream_t s) {
+  const DssRange g = range(side, e_begin, e_end, ap_base);
   const int nb = dss_blocks(g);
+  const int64_t work = (ap_end - ap_base) * int64_t(degree + 1) * (degree + 1);
+  const int64_t want = (work + kDssThreads - 1) / kDssThreads;
+  const int np = int(want < 1 ? 1 : (want < int64_t(sm_count()) * 16 ? want
+                                                                     : int64_t(sm_count()) * 16));
   cudaError_t err;
 #define HX_CALL(N)                                                                           \
-  cg_update_masked_kernel<N><<<nb, kDssThreads, 0, s>>>(x, p, r, w, g, mask, rr, pap, part); \
+  dss_pass_kernel<N, 0><<<np, kDssThreads, 0, s>>>(ap, side, ap_base, ap_end);               \
+  if ((err = cudaGetLastError()) != cudaSuccess) return err;                                \
+  dss_pass_kernel<N, 1><<<np, kDssThreads, 0, s>>>(ap, side, ap_base, ap_end);               \
+  if ((err = cudaGetLastError()) != cudaSuccess) return err;                                \
+  dss_pass_kernel<N, 2><<<np, kDssThreads, 0, s>>>(ap, side, ap_base, ap_end);               \
+  if ((err = cudaGetLastError()) != cudaSuccess) return err;                                \
+  cg_update_assembled_kernel<N><<<nb, kDssThreads, 0, s>>>(x, p, r, ap, g, mask, rr, pap,    \
+                                                           part);                           \
   if ((err = cudaGetLastError()) != cudaSuccess) return err;                                \
   return launch_sum(part, nb, rr_new, s);
   HX_DSS_DISPATCH(HX_CALL)

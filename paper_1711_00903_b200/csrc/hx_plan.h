@@ -72,11 +72,11 @@ cudaError_t launch_cg_update_dss(double* x, const double* p, double* r, const do
 
 cudaError_t launch_dss_inplace(double* u, int side, int degree, int64_t lo, int64_t hi,
                                cudaStream_t s);
-cudaError_t launch_cg_update_masked(double* x, const double* p, double* r, const double* w,
-                                    int side, int degree, int mask, int64_t e_begin,
-                                    int64_t e_end, int64_t w_base, const double* rr,
-                                    const double* pap, double* part, double* rr_new,
-                                    cudaStream_t s);
+cudaError_t launch_cg_update_assembled(double* x, const double* p, double* r, double* ap,
+                                       int side, int degree, int mask, int64_t e_begin,
+                                       int64_t e_end, int64_t ap_base, int64_t ap_end,
+                                       const double* rr, const double* pap, double* part,
+                                       double* rr_new, cudaStream_t s);
 
 int sm_count();
 

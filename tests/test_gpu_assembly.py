@@ -168,6 +168,46 @@ def test_inplace_separable_dss_matches_oracle(side, deg):
             np.testing.assert_array_equal(sh.own(pad).cpu().numpy(), got[sh.lo:sh.hi])
 
 
+@pytest.mark.parametrize("world", [1, 2])
+def test_cg_update_assembled_kernel(world):
+    """hx_cg_update_assembled on each rank's range (y/z passes in place on the
+    halo buffer, x pass fused): x += a p, r -= a mask QQ^T ap, <r,r>_w."""
+    from paper_1711_00903_b200.cg import AssembledShard
+
+    side, deg = 4, 3
+    n3 = (deg + 1) ** 3
+    rng = np.random.default_rng(21)
+    E = side ** 3
+    x, p, r, ap = rng.standard_normal((4, E, n3))
+    rr, pap = 2.5, 1.25
+    alpha = rr / pap
+    w_ref = orc.dss(ap, side, deg, mask=True)
+    x_ref = x + alpha * p
+    r_ref = r - alpha * w_ref
+    L = _native.lib()
+    part = torch.empty(L.hx_energy_partials(), dtype=torch.float64, device="cuda")
+    total = 0.0
+    for rank in range(world):
+        sh = AssembledShard(side, deg, rank, world)
+        dev = {k: torch.from_numpy(v[sh.lo:sh.hi].copy()).cuda()
+               for k, v in (("x", x), ("p", p), ("r", r))}
+        ap_pad = torch.from_numpy(ap[sh.base:sh.top].copy()).cuda()
+        rrd = torch.tensor([rr], dtype=torch.float64, device="cuda")
+        papd = torch.tensor([pap], dtype=torch.float64, device="cuda")
+        out = torch.zeros(1, dtype=torch.float64, device="cuda")
+        _native.check(L.hx_cg_update_assembled(
+            _native.ptr(dev["x"]), _native.ptr(dev["p"]), _native.ptr(dev["r"]),
+            _native.ptr(ap_pad), side, deg, 1, sh.lo, sh.hi, sh.base, sh.top, _native.ptr(rrd),
+            _native.ptr(papd), _native.ptr(part), part.numel(), _native.ptr(out), None))
+        np.testing.assert_allclose(dev["x"].cpu().numpy(), x_ref[sh.lo:sh.hi], rtol=0,
+                                   atol=1e-14)
+        np.testing.assert_allclose(dev["r"].cpu().numpy(), r_ref[sh.lo:sh.hi], rtol=1e-13,
+                                   atol=1e-13)
+        total += float(out)
+    want = float(np.sum(r_ref ** 2 / orc.multiplicity(side, deg)))
+    assert abs(total - want) <= 1e-12 * want
+
+
 def test_dss_argument_errors():
     u = torch.zeros(8 * 27, dtype=torch.float64, device="cuda")
     with pytest.raises(ValueError):
