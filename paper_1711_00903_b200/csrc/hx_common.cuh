@@ -323,6 +323,10 @@ constexpr int smem_doubles() {
   for (int b = 0; b < int(sizeof(C::EBUF) / sizeof(int)); ++b) s += C::EBUF[b];
   s *= C::EPB;
   if (C::QS > 0) s += 2 + C::EPB * (N + 1) * C::QS;
+#ifndef HX_BP1_XDB
+#define HX_BP1_XDB 0
+#endif
+  if (BP == kBP1 && HX_BP1_XDB) s += C::EPB * C::EBUF[0];  // second X buffer (hx_bp1.cu)
   return s;
 }
 
