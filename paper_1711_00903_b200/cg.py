@@ -29,10 +29,22 @@ class CGResult:
     residual_norms: list = field(default_factory=list)  # ||r|| at each check
 
 
+def _host_staged(t, group):
+    """gloo (the CPU test backend) takes host tensors: stage device data
+    through the host there; NCCL works on the device tensors directly."""
+    import torch.distributed as dist
+    return t.is_cuda and dist.get_backend(group) == "gloo"
+
+
 def _allreduce(t, group):
     import torch.distributed as dist
     if dist.is_available() and dist.is_initialized():
-        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+        if _host_staged(t, group):
+            h = t.cpu()
+            dist.all_reduce(h, op=dist.ReduceOp.SUM, group=group)
+            t.copy_(h)
+        else:
+            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
 
 
 class CGWorkspace:
@@ -201,20 +213,28 @@ class AssembledShard:
             return
         import torch.distributed as dist
 
-        ops = []
         o0, o1 = self.lo - self.base, self.hi - self.base
-        if self.rank > 0:  # halo below: [base, lo) belongs to rank - 1
-            ops.append(dist.P2POp(dist.irecv, pad[:o0], self.rank - 1, self.group))
-            n_send = min(self.halo, self.n_own)
-            ops.append(dist.P2POp(dist.isend, pad[o0:o0 + n_send].contiguous(), self.rank - 1,
-                                  self.group))
-        if self.rank < self.world_size - 1:  # halo above: [hi, top) belongs to rank + 1
-            ops.append(dist.P2POp(dist.irecv, pad[o1:], self.rank + 1, self.group))
-            n_send = min(self.halo, self.n_own)
-            ops.append(dist.P2POp(dist.isend, pad[o1 - n_send:o1].contiguous(), self.rank + 1,
-                                  self.group))
+        n_send = min(self.halo, self.n_own)
+        # (peer, receive view, send view): halo below from / own head to rank-1,
+        # halo above from / own tail to rank+1
+        links = []
+        if self.rank > 0:
+            links.append((self.rank - 1, pad[:o0], pad[o0:o0 + n_send]))
+        if self.rank < self.world_size - 1:
+            links.append((self.rank + 1, pad[o1:], pad[o1 - n_send:o1]))
+        staged = _host_staged(pad, self.group)
+        ops, recvs = [], []
+        for peer, rview, sview in links:
+            rbuf = rview.new_empty(rview.shape, device="cpu") if staged else rview
+            if rbuf is not rview or not rview.is_contiguous():
+                recvs.append((rview, rbuf))
+            sbuf = sview.cpu() if staged else sview.contiguous()
+            ops.append(dist.P2POp(dist.irecv, rbuf, peer, self.group))
+            ops.append(dist.P2POp(dist.isend, sbuf, peer, self.group))
         for req in dist.batch_isend_irecv(ops):
             req.wait()
+        for rview, rbuf in recvs:
+            rview.copy_(rbuf)
 
 
 def gather_scatter(u, side, degree, mask_boundary=False, out=None, stream=None, shard=None):

@@ -214,3 +214,54 @@ def test_dss_argument_errors():
         gather_scatter(u, 3, 2)            # wrong size for the mesh
     with pytest.raises(ValueError):
         gather_scatter(u, 2, 2, out=u)     # in-place is rejected
+
+
+def _sharded_cg_worker(rank, world, port, result_path):
+    import os
+    import torch.distributed as dist
+
+    from paper_1711_00903_b200.cg import AssembledShard
+    from paper_1711_00903_b200.shard import ShardedOperator
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)  # both ranks share the one GPU (gloo moves the scalars/halos)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        side, deg = 4, 3
+        mesh = hx.build_cube_mesh(side, 2.0)
+        sh = AssembledShard(side, deg, rank, world)
+        op = ShardedOperator(hx.BP35, deg, mesh, lam=0.0, rank=rank, world_size=world).op
+        b = np.random.default_rng(3).standard_normal((side ** 3, (deg + 1) ** 3))
+        res = cg_solve_assembled(op, side, torch.from_numpy(b[sh.lo:sh.hi].copy()).cuda(),
+                                 tol=1e-12, shard=sh)
+        np.save(f"{result_path}.{rank}.npy", res.x.cpu().numpy())
+        np.save(f"{result_path}.{rank}.it.npy", np.array([res.iterations, res.converged]))
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_assembled_cg_two_ranks_on_one_gpu(tmp_path):
+    """The multi-GPU assembled CG end to end -- kernels over element ranges,
+    halo exchange, all-reduced scalars -- as two ranks sharing the GPU (gloo
+    carries the exchange here, NCCL on a multi-GPU node): the gathered
+    solution equals the one-rank solve."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    base = str(tmp_path / "x")
+    mp.spawn(_sharded_cg_worker, args=(2, port, base), nprocs=2, join=True)
+    x2 = np.concatenate([np.load(f"{base}.{r}.npy") for r in range(2)])
+    its = [np.load(f"{base}.{r}.it.npy") for r in range(2)]
+    side, deg = 4, 3
+    mesh = hx.build_cube_mesh(side, 2.0)
+    op = hx.make_operator(hx.BP35, deg, mesh, lam=0.0)
+    b = np.random.default_rng(3).standard_normal((side ** 3, (deg + 1) ** 3))
+    ref = cg_solve_assembled(op, side, torch.from_numpy(b).cuda(), tol=1e-12)
+    assert all(bool(i[1]) for i in its) and its[0][0] == its[1][0]
+    assert orc.rel_l2(x2, ref.x.cpu().numpy()) <= 1e-10
