@@ -34,6 +34,10 @@
 #define HX_BP1_XDB 0
 #endif
 
+#ifndef HX_BP1_SPLIT_FULL
+#define HX_BP1_SPLIT_FULL 0
+#endif
+
 // HX_BP1_SHARED_FOLD: apply I^T from I's own fold (fold_apply_T) instead of
 // a second coefficient set, so S3's I_t and I_t^T read the same constants.
 #ifndef HX_BP1_SHARED_FOLD
@@ -121,9 +125,11 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT, HX_MINB_BP1_OF(N))
 
   double en = 0.0;  // this thread's share of <q, A q> (ENERGY)
   int parity = 0;   // which X buffer this tile uses (XDB)
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, parity ^= 1) {
+  // The tile body takes the tile's element count; full tiles (all but the
+  // last) pass the compile-time EPB so the per-line `el >= ne` guards fold
+  // away (HX_BP1_SPLIT_FULL).
+  auto tile_body = [&](const int64_t tile, const int ne) __attribute__((always_inline)) {
     const int64_t e0 = tile * EPB;
-    const int ne = int(min64(EPB, p.n_el - e0));
     double* const Xt = X + (XDB && parity ? EPB * EX : 0);
     if (tid == 0) {
       const int64_t nt = tile + gridDim.x;
@@ -252,6 +258,13 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT, HX_MINB_BP1_OF(N))
       for (int t = 0; t < n; ++t) st_stream(dst + t * n, y[t]);
     });
     if constexpr (!XDB) __syncthreads();  // X is rewritten by the next tile's S1
+  };
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, parity ^= 1) {
+    const int ne = int(min64(EPB, p.n_el - tile * EPB));
+    if (HX_BP1_SPLIT_FULL && ne == EPB)
+      tile_body(tile, EPB);
+    else
+      tile_body(tile, ne);
   }
   if constexpr (ENERGY) {
     const double sum = block_sum<C::NT>(en, X);
