@@ -156,17 +156,12 @@ int hx_cg_direction(double* p, const double* r, int64_t n, const double* rr_new,
  *   hx_dot_dss:       *result = sum u v / multiplicity over the range
  *                     (= <u_G, v_G> for continuous representatives, summed
  *                     over ranks)
- *   hx_cg_update_dss: hx_cg_update with r -= alpha mask Q Q^T ap and the
- *                     multiplicity-weighted <r, r>                             */
+ * The per-iteration assembled update is hx_cg_update_assembled (below).     */
 int hx_dss(const double* in, double* out, int side, int degree, int mask_boundary,
            int64_t e_begin, int64_t e_end, int64_t in_base, void* stream);
 int hx_dot_dss(const double* u, const double* v, int side, int degree, int64_t e_begin,
                int64_t e_end, double* partials, int64_t n_partials, double* result,
                void* stream);
-int hx_cg_update_dss(double* x, const double* p, double* r, const double* ap, int side,
-                     int degree, int mask_boundary, int64_t e_begin, int64_t e_end,
-                     int64_t ap_base, const double* rr, const double* pap, double* partials,
-                     int64_t n_partials, double* rr_new, void* stream);
 
 /* Separable in-place gather-scatter: u (a buffer holding elements
  * [buf_begin, buf_end)) <- Q Q^T u as three per-axis face passes (each copy of

@@ -48,8 +48,6 @@ SIGNATURES = {
                           _c.c_int64, _P]),
     "hx_dot_dss": (_c.c_int, [_P, _P, _c.c_int, _c.c_int, _c.c_int64, _c.c_int64, _P,
                               _c.c_int64, _P, _P]),
-    "hx_cg_update_dss": (_c.c_int, [_P, _P, _P, _P, _c.c_int, _c.c_int, _c.c_int, _c.c_int64,
-                                    _c.c_int64, _c.c_int64, _P, _P, _P, _c.c_int64, _P, _P]),
     "hx_dss_inplace": (_c.c_int, [_P, _c.c_int, _c.c_int, _c.c_int64, _c.c_int64, _P]),
     "hx_cg_update_assembled": (_c.c_int, [_P, _P, _P, _P, _c.c_int, _c.c_int, _c.c_int,
                                           _c.c_int64, _c.c_int64, _c.c_int64, _c.c_int64,

@@ -341,20 +341,6 @@ int hx_dot_dss(const double* u, const double* v, int side, int degree, int64_t e
                                     static_cast<cudaStream_t>(stream)));
 }
 
-int hx_cg_update_dss(double* x, const double* p, double* r, const double* ap, int side,
-                     int degree, int mask, int64_t e_begin, int64_t e_end, int64_t ap_base,
-                     const double* rr, const double* pap, double* partials,
-                     int64_t n_partials, double* rr_new, void* stream) {
-  if (!dss_args_ok(side, degree, e_begin, e_end) || ap_base < 0 || ap_base > e_begin)
-    return HX_EINVAL;
-  if (!rr || !pap || !partials || !rr_new) return HX_EINVAL;
-  if (e_end > e_begin && (!x || !p || !r || !ap)) return HX_EINVAL;
-  if (n_partials < hx_energy_partials()) return HX_EINVAL;
-  return cuda_status(launch_cg_update_dss(x, p, r, ap, side, degree, mask != 0, e_begin, e_end,
-                                          ap_base, rr, pap, partials, rr_new,
-                                          static_cast<cudaStream_t>(stream)));
-}
-
 int hx_dss_inplace(double* u, int side, int degree, int64_t buf_begin, int64_t buf_end,
                    void* stream) {
   if (!dss_args_ok(side, degree, buf_begin, buf_end)) return HX_EINVAL;

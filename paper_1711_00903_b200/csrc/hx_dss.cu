@@ -24,7 +24,7 @@
 // Assembled CG keeps every vector in element-local storage as its continuous
 // representative u_L = Q u_G.  Then
 //   <p_G, A_G p_G> = <p_L, A_L p_L>                 (fused into the matvec)
-//   A_G p_G        -> mask dss(A_L p_L)             (fused into the update)
+//   A_G p_G        -> mask dss(A_L p_L)             (face passes in place on A p)
 //   <r_G, r_G>     = sum_L r_L^2 / multiplicity      (fused into the update)
 #include "hx_common.cuh"
 #include "hx_plan.h"
@@ -155,29 +155,6 @@ __global__ void __launch_bounds__(kDssThreads)
   double s = 0.0;
   for_nodes<N>(g, [&](const NodeRef& r, int64_t idx) {
     s = fma(u[idx], v[idx] * inv_mult<N>(r, g.side), s);
-  });
-  s = block_sum<kDssThreads>(s, scratch);
-  if (threadIdx.x == 0) part[blockIdx.x] = s;
-}
-
-// alpha = rr / pAp;  x += alpha p;  r -= alpha mask dss(ap);  partials of
-// sum r^2 / multiplicity.  The assembled A p is never written to memory.
-template <int N>
-__global__ void __launch_bounds__(kDssThreads)
-    cg_update_dss_kernel(double* __restrict__ x, const double* __restrict__ p,
-                         double* __restrict__ r, const double* __restrict__ ap, DssRange g,
-                         int mask, const double* __restrict__ rr,
-                         const double* __restrict__ pap, double* __restrict__ part) {
-  __shared__ double scratch[kDssThreads / 32];
-  const double alpha = rr[0] / pap[0];
-  double s = 0.0;
-  for_nodes<N>(g, [&](const NodeRef& nr, int64_t idx) {
-    const double w =
-        (mask && on_boundary<N>(nr, g.side)) ? 0.0 : gather_sum<N>(ap, nr, g.side, g.base);
-    x[idx] = fma(alpha, p[idx], x[idx]);
-    const double ri = fma(-alpha, w, r[idx]);
-    r[idx] = ri;
-    s = fma(ri, ri * inv_mult<N>(nr, g.side), s);
   });
   s = block_sum<kDssThreads>(s, scratch);
   if (threadIdx.x == 0) part[blockIdx.x] = s;
@@ -342,22 +319,6 @@ cudaError_t launch_dot_dss(const double* u, const double* v, int side, int degre
   dot_dss_kernel<N><<<nb, kDssThreads, 0, s>>>(u, v, g, part);    \
   if ((err = cudaGetLastError()) != cudaSuccess) return err;      \
   return launch_sum(part, nb, result, s);
-  HX_DSS_DISPATCH(HX_CALL)
-#undef HX_CALL
-}
-
-cudaError_t launch_cg_update_dss(double* x, const double* p, double* r, const double* ap,
-                                 int side, int degree, int mask, int64_t e_begin,
-                                 int64_t e_end, int64_t ap_base, const double* rr,
-                                 const double* pap, double* part, double* rr_new,
-                                 cudaStream_t s) {
-  const DssRange g = range(side, e_begin, e_end, ap_base);
-  const int nb = dss_blocks(g);
-  cudaError_t err;
-#define HX_CALL(N)                                                                            \
-  cg_update_dss_kernel<N><<<nb, kDssThreads, 0, s>>>(x, p, r, ap, g, mask, rr, pap, part);   \
-  if ((err = cudaGetLastError()) != cudaSuccess) return err;                                 \
-  return launch_sum(part, nb, rr_new, s);
   HX_DSS_DISPATCH(HX_CALL)
 #undef HX_CALL
 }

@@ -64,11 +64,6 @@ cudaError_t launch_dss(const double* in, double* out, int side, int degree, int 
 cudaError_t launch_dot_dss(const double* u, const double* v, int side, int degree,
                            int64_t e_begin, int64_t e_end, double* part, double* result,
                            cudaStream_t s);
-cudaError_t launch_cg_update_dss(double* x, const double* p, double* r, const double* ap,
-                                 int side, int degree, int mask, int64_t e_begin,
-                                 int64_t e_end, int64_t ap_base, const double* rr,
-                                 const double* pap, double* part, double* rr_new,
-                                 cudaStream_t s);
 
 cudaError_t launch_dss_inplace(double* u, int side, int degree, int64_t lo, int64_t hi,
                                cudaStream_t s);
