@@ -1,10 +1,12 @@
 // C ABI entry points (include/hexbench_b200.h).  Thin: validate, dispatch to
 // the per-operator launchers, translate CUDA errors into HX_ECUDA.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <new>
+#include <vector>
 
 #include "hx_common.cuh"
 #include "hx_plan.h"
@@ -128,7 +130,7 @@ void hx_plan_destroy(hx_plan* P) {
   if (P->pipe_ready) {
     for (int i = 0; i < 3; ++i) {
       cudaStreamDestroy(P->pipe[i]);
-      for (int j = 0; j < 2; ++j) cudaEventDestroy(P->ev[i][j]);
+      for (int j = 0; j < hx_host_slots; ++j) cudaEventDestroy(P->ev[i][j]);
     }
   }
   delete P;
@@ -206,7 +208,32 @@ int hx_interp_elements(int degree, const double* interp, int project, const doub
 int64_t hx_apply_host_workspace(const hx_plan* P, int64_t chunk_el) {
   if (!P || chunk_el <= 0) return -1;
   const int64_t n3 = int64_t(P->n) * P->n * P->n;
-  return 2 /*slots*/ * 2 /*q,out*/ * chunk_el * n3 * int64_t(sizeof(double));
+  return hx_host_slots * 2 /*q,out*/ * chunk_el * n3 * int64_t(sizeof(double));
+}
+
+// Chunk sizes of the host pipeline: ramp up from chunk_el/8 by doubling,
+// full chunks in the middle, ramp down at the end.  The pipeline's fill (the
+// first H2D runs alone) and drain (the last D2H runs alone) then cost a small
+// chunk each instead of a full one.  Falls back to uniform chunks when the
+// problem is too small for the ramps.
+static std::vector<int64_t> chunk_schedule(int64_t n_el, int64_t chunk_el) {
+  std::vector<int64_t> head;
+  int64_t ramp = 0;
+  for (int64_t c = std::max<int64_t>(1, chunk_el / 8); c < chunk_el; c *= 2) {
+    head.push_back(c);
+    ramp += c;
+  }
+  std::vector<int64_t> out;
+  if (head.empty() || n_el <= 2 * ramp + chunk_el) {
+    for (int64_t e = 0; e < n_el; e += chunk_el) out.push_back(std::min(chunk_el, n_el - e));
+    return out;
+  }
+  out = head;
+  const int64_t mid = n_el - 2 * ramp;
+  const int64_t k = (mid + chunk_el - 1) / chunk_el;
+  for (int64_t i = 0; i < k; ++i) out.push_back(mid / k + (i < mid % k ? 1 : 0));
+  out.insert(out.end(), head.rbegin(), head.rend());
+  return out;
 }
 
 int hx_apply_host(const hx_plan* Pc, const double* q_host, const double* factors,
@@ -222,7 +249,7 @@ int hx_apply_host(const hx_plan* Pc, const double* q_host, const double* factors
     for (int i = 0; i < 3; ++i) {
       if ((err = cudaStreamCreateWithFlags(&P->pipe[i], cudaStreamNonBlocking)) != cudaSuccess)
         return cuda_status(err);
-      for (int j = 0; j < 2; ++j)
+      for (int j = 0; j < hx_host_slots; ++j)
         if ((err = cudaEventCreateWithFlags(&P->ev[i][j], cudaEventDisableTiming)) !=
             cudaSuccess)
           return cuda_status(err);
@@ -230,13 +257,14 @@ int hx_apply_host(const hx_plan* Pc, const double* q_host, const double* factors
     P->pipe_ready = true;
   }
   const int64_t n3 = int64_t(P->n) * P->n * P->n;
-  double* wq[2];
-  double* wo[2];
+  constexpr int S = hx_host_slots;
+  double* wq[S];
+  double* wo[S];
   double* base = static_cast<double*>(work);
-  wq[0] = base;
-  wq[1] = base + chunk_el * n3;
-  wo[0] = base + 2 * chunk_el * n3;
-  wo[1] = base + 3 * chunk_el * n3;
+  for (int i = 0; i < S; ++i) {
+    wq[i] = base + int64_t(i) * chunk_el * n3;
+    wo[i] = base + int64_t(S + i) * chunk_el * n3;
+  }
   cudaStream_t s_in = P->pipe[0], s_k = P->pipe[1], s_out = P->pipe[2];
   cudaEvent_t* e_in = P->ev[0];
   cudaEvent_t* e_k = P->ev[1];
@@ -249,17 +277,18 @@ int hx_apply_host(const hx_plan* Pc, const double* q_host, const double* factors
   cudaStreamWaitEvent(s_in, start, 0);
   cudaStreamWaitEvent(s_k, start, 0);
   cudaStreamWaitEvent(s_out, start, 0);
-  const int64_t nchunks = (n_el + chunk_el - 1) / chunk_el;
+  const std::vector<int64_t> sched = chunk_schedule(n_el, chunk_el);
+  const int64_t nchunks = int64_t(sched.size());
+  int64_t e0 = 0;
   for (int64_t c = 0; c < nchunks; ++c) {
-    const int slot = int(c & 1);
-    const int64_t e0 = c * chunk_el;
-    const int64_t ne = std::min(chunk_el, n_el - e0);
+    const int slot = int(c % S);
+    const int64_t ne = sched[c];
     const size_t bytes = size_t(ne * n3) * sizeof(double);
-    if (c >= 2) cudaStreamWaitEvent(s_in, e_k[slot], 0);  // kernel c-2 done reading wq[slot]
+    if (c >= S) cudaStreamWaitEvent(s_in, e_k[slot], 0);  // kernel c-S done reading wq[slot]
     cudaMemcpyAsync(wq[slot], q_host + e0 * n3, bytes, cudaMemcpyHostToDevice, s_in);
     cudaEventRecord(e_in[slot], s_in);
     cudaStreamWaitEvent(s_k, e_in[slot], 0);
-    if (c >= 2) cudaStreamWaitEvent(s_k, e_out[slot], 0);  // D2H c-2 done with wo[slot]
+    if (c >= S) cudaStreamWaitEvent(s_k, e_out[slot], 0);  // D2H c-S done with wo[slot]
     if ((err = launch(*P, wq[slot], factors + e0 * P->elem_stride, wo[slot], ne, flag, s_k)) !=
         cudaSuccess) {
       cudaEventDestroy(start);
@@ -269,9 +298,10 @@ int hx_apply_host(const hx_plan* Pc, const double* q_host, const double* factors
     cudaStreamWaitEvent(s_out, e_k[slot], 0);
     cudaMemcpyAsync(out_host + e0 * n3, wo[slot], bytes, cudaMemcpyDeviceToHost, s_out);
     cudaEventRecord(e_out[slot], s_out);
+    e0 += ne;
   }
-  cudaStreamWaitEvent(caller, e_out[(nchunks - 1) & 1], 0);
-  if (nchunks >= 2) cudaStreamWaitEvent(caller, e_out[nchunks & 1], 0);
+  // D2H is in order on one stream: its last chunk done means all are
+  cudaStreamWaitEvent(caller, e_out[(nchunks - 1) % S], 0);
   cudaEventDestroy(start);
   return cuda_status(cudaGetLastError());
 }

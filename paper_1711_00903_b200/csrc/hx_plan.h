@@ -12,6 +12,10 @@ constexpr int kMaxQ = 17;  // N <= 15 -> at most N+2 points per axis
 
 }  // namespace hx
 
+// device buffer slots of the host pipeline (hx_apply_host): H2D, kernel and
+// D2H of up to this many chunks are in flight at once
+constexpr int hx_host_slots = 3;
+
 struct hx_plan {
   int bp;       // HX_BP1 / HX_BP35 / HX_BP3
   int degree;   // N
@@ -27,7 +31,7 @@ struct hx_plan {
   int64_t elem_stride;    // doubles per element (n_slots * slot_stride)
   // lazily created resources for the host-buffer (end-to-end) path
   cudaStream_t pipe[3];
-  cudaEvent_t ev[3][2];
+  cudaEvent_t ev[3][hx_host_slots];
   bool pipe_ready;
 };
 
