@@ -86,8 +86,9 @@ int hx_apply(const hx_plan* plan, const double* q, const double* factors, double
              int64_t n_el, int* status_flag, void* stream);
 
 /* End-to-end variant on HOST q / out (page-locked for full overlap): chunks of
- * up to `chunk_el` elements (ramped up and down at the ends) are copied in, applied and copied back on a three-stream
- * pipeline so PCIe transfers overlap the kernel.  `work` is a device buffer of
+ * up to `chunk_el` elements (ramped up and down at the ends) are copied in,
+ * applied and copied back on a three-stream pipeline with three buffer slots,
+ * so PCIe transfers in both directions overlap each other and the kernel.  `work` is a device buffer of
  * at least hx_apply_host_workspace(plan, chunk_el) bytes; `stream` is made to
  * wait for the whole pipeline.                                              */
 int64_t hx_apply_host_workspace(const hx_plan* plan, int64_t chunk_el);
