@@ -34,6 +34,13 @@ def _degrees(text):
     return list(range(lo, hi + 1))
 
 
+def _spacer():
+    """Queue ~100 us of GPU work before a timed launch so host launch latency
+    is not timed (see bench.gpu_spacer)."""
+    import torch
+    torch.cuda._sleep(200_000)
+
+
 def device_copy_bandwidth(nbytes, trials=10):
     """Mean read+write bandwidth of a D2D copy of nbytes."""
     import torch
@@ -44,6 +51,7 @@ def device_copy_bandwidth(nbytes, trials=10):
     rates = []
     for _ in range(trials):
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        _spacer()
         s.record()
         b.copy_(a)
         e.record()
@@ -84,6 +92,7 @@ def bench_runs(bps, degrees, side, variant="fused", lam=1.0, repeats=10, seed=0,
             times = []
             for _ in range(repeats):
                 s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                _spacer()
                 s.record()
                 apply_device(op, q, out)
                 e.record()

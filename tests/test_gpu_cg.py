@@ -109,3 +109,26 @@ def test_report_bench_schema():
         assert r["counted_global_bytes"] == r["model_bytes"]
         assert r["wall_time_median_s"] > 0 and r["gdof_per_s"] > 0
     assert "r_shared_flops_per_s" in runs[0] and "r_shared_flops_per_s" not in runs[1]
+
+
+def test_report_cli_json_and_csv(tmp_path):
+    """`python -m paper_1711_00903_b200.report {bench,roofline}` (the reference
+    cli.py:235-347 commands) write the JSON / CSV schemas."""
+    import csv
+    import json
+
+    from paper_1711_00903_b200.report import main
+
+    out = tmp_path / "bench.json"
+    assert main(["bench", "--bp", "3.5", "--degrees", "2", "--elements", "2", "--repeats", "2",
+                 "--out", str(out)]) == 0
+    payload = json.loads(out.read_text())
+    assert payload["command"] == "bench" and len(payload["runs"]) == 1
+    assert payload["runs"][0]["bp"] == hx.BP35
+    out = tmp_path / "roof.csv"
+    assert main(["roofline", "--bp", "1.0", "--degrees", "1..3", "--elements", "2",
+                 "--bandwidth", "6000", "--format", "csv", "--out", str(out)]) == 0
+    rows = list(csv.reader(out.open()))
+    assert rows[0] == ["bp", "N", "F", "bytes", "R_global", "R_shared"]
+    assert [int(r[1]) for r in rows[1:]] == [1, 2, 3]
+    assert all(float(r[4]) > 0 and float(r[5]) > 0 for r in rows[1:])
