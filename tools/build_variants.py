@@ -26,17 +26,22 @@ from paper_1711_00903_b200 import build as native_build  # noqa: E402
 VARIANTS = os.path.join(ROOT, "paper_1711_00903_b200", "variants")
 
 
+BPS = {"bp1": gen_layouts.BP1, "bp35": gen_layouts.BP35, "bp3": gen_layouts.BP3}
+
+
 def parse(name):
-    m = re.fullmatch(r"t(\d+)_m(\d+)(?:_q(\d))?", name)
+    """[bp1_|bp35_|bp3_]t<T>_m<M>[_q<Q>] -> (bps, T, M, Q); BP1.0 by default."""
+    m = re.fullmatch(r"(?:(bp1|bp35|bp3)_)?t(\d+)_m(\d+)(?:_q(\d))?", name)
     if not m:
-        raise SystemExit(f"bad variant name {name!r} (want t<T>_m<M>[_q<Q>])")
-    return int(m.group(1)), int(m.group(2)), int(m.group(3) or 0)
+        raise SystemExit(f"bad variant name {name!r} (want [bpX_]t<T>_m<M>[_q<Q>])")
+    bps = (BPS[m.group(1)],) if m.group(1) else (gen_layouts.BP1,)
+    return bps, int(m.group(2)), int(m.group(3)), int(m.group(4) or 0)
 
 
-def build_variant(name, bps=(gen_layouts.BP1,)):
-    """The variant's shape applies to the kernels in `bps`; the others keep
-    the committed policy."""
-    t, mb, q = parse(name)
+def build_variant(name):
+    """The variant's shape applies to the kernel its name selects (BP1.0 by
+    default); the others keep the committed policy."""
+    bps, t, mb, q = parse(name)
     pol_path = os.path.join(HERE, "tune_policy.json")
     policy = gen_layouts.load_policy(pol_path) if os.path.exists(pol_path) else {}
     for bp in bps:
