@@ -83,7 +83,19 @@ def test_plan_create_rejects_bad_arguments():
     assert lib.hx_plan_create(_native.HX_BP3, 3, 0.0, None, ptrs[1], ptrs[2], ptrs[3],
                               ctypes.byref(h)) == _native.HX_EINVAL
     assert lib.hx_plan_create(_native.HX_BP3, 3, 0.0, *ptrs, None) == _native.HX_EINVAL
+    # matrices that are not (anti-)centro-symmetric would be mis-applied by the
+    # folded kernels: rejected
+    bad_i = arrs[0].copy()
+    bad_i[0, 0] += 1e-3
+    assert lib.hx_plan_create(_native.HX_BP3, 3, 0.0, bad_i.ctypes.data, *ptrs[1:],
+                              ctypes.byref(h)) == _native.HX_EINVAL
+    bad_d = arrs[1].copy()
+    bad_d[1, 2] += 1e-3
+    assert lib.hx_plan_create(_native.HX_BP3, 3, 0.0, ptrs[0], bad_d.ctypes.data, *ptrs[2:],
+                              ctypes.byref(h)) == _native.HX_EINVAL
     assert lib.hx_plan_create(_native.HX_BP3, 3, 0.5, *ptrs, ctypes.byref(h)) == _native.HX_OK
+    # pointers to doubles must be 8-byte aligned (checked before any launch)
+    assert lib.hx_apply(h, 8, 16, 3, 1, None, None) == _native.HX_EINVAL
     assert lib.hx_apply(h, None, None, None, -1, None, None) == _native.HX_EINVAL
     assert lib.hx_apply(h, None, None, None, 4, None, None) == _native.HX_EINVAL
     assert lib.hx_apply(None, None, None, None, 0, None, None) == _native.HX_EINVAL
