@@ -429,13 +429,43 @@ def cg_assembled_report(side=32, iters=20, warmup=3):
     ms = (timed(iters) - timed(0)) / iters
     per_el = hx.traffic(op.bp, op.degree).bytes_per_element + 9 * 8 * op.n_p
     unique = (side * DEGREE + 1) ** 3
+    small = small_mesh_cg_graph()
     return {"bp": op.bp, "degree": op.degree, "n_el": op.n_el, "side": side,
             "global_dofs": unique, "ms_per_iteration": ms,
             "gdof_iterations_per_s": op.n_el * op.n_p / (ms * 1e-3) / 1e9,
             "global_gdof_iterations_per_s": unique / (ms * 1e-3) / 1e9,
             "hbm_bytes_per_iteration": per_el * op.n_el,
             "achieved_gb_per_s": per_el * op.n_el / (ms * 1e-3) / 1e9,
-            "kernels_per_iteration": 5}
+            "kernels_per_iteration": 5, "small_mesh_cuda_graph": small}
+
+
+def small_mesh_cg_graph(side=8, iters=200):
+    """Launch-bound regime: assembled CG on a side-8 cube (512 elements, N=7),
+    eager (~7 launches per iteration from Python) vs the iteration blocks
+    captured once as a CUDA graph (AssembledCG(graph=True)).  Wall
+    clock per iteration, including the host reads of the residual every 10
+    iterations."""
+    import time
+
+    import torch
+    import paper_1711_00903_b200 as hx
+    from paper_1711_00903_b200.cg import AssembledCG
+
+    mesh = hx.build_cube_mesh(side, 2.0)
+    op = hx.make_operator(hx.BP35, DEGREE, mesh, lam=0.0)
+    b = torch.randn(op.n_el, op.n_p, dtype=torch.float64, device="cuda")
+    res = {}
+    for name, graph in (("eager", False), ("graph", True)):
+        solver = AssembledCG(op, side, graph=graph)  # the graph is captured here, once
+        solver.solve(b, tol=0.0, maxiter=20)  # warm-up
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        solver.solve(b, tol=0.0, maxiter=iters)
+        torch.cuda.synchronize()
+        res[f"{name}_us_per_iteration"] = (time.perf_counter() - t0) / iters * 1e6
+    res["n_el"] = mesh.n_el
+    res["speedup"] = res["eager_us_per_iteration"] / res["graph_us_per_iteration"]
+    return res
 
 
 def unfused_pass_bytes(bp, deg=DEGREE):

@@ -265,3 +265,18 @@ def test_sharded_assembled_cg_two_ranks_on_one_gpu(tmp_path):
     ref = cg_solve_assembled(op, side, torch.from_numpy(b).cuda(), tol=1e-12)
     assert all(bool(i[1]) for i in its) and its[0][0] == its[1][0]
     assert orc.rel_l2(x2, ref.x.cpu().numpy()) <= 1e-10
+
+
+def test_graphed_assembled_cg_is_bitwise_the_eager_one():
+    """graph=True replays the captured iteration blocks: same iterates bit for
+    bit as the eager loop (same kernels, same order, deterministic sums)."""
+    side, deg = 3, 4
+    mesh = hx.build_cube_mesh(side, 2.0)
+    op = hx.make_operator(hx.BP35, deg, mesh, lam=0.0)
+    b = torch.from_numpy(np.random.default_rng(8).standard_normal((mesh.n_el, op.n_p))).cuda()
+    eager = cg_solve_assembled(op, side, b, tol=1e-11, check_every=10)
+    graphed = cg_solve_assembled(op, side, b, tol=1e-11, check_every=10, graph=True)
+    assert eager.converged and graphed.converged
+    assert graphed.iterations == -(-eager.iterations // 10) * 10
+    # the eager solve stopped at its check; the graphed one at the same check
+    np.testing.assert_array_equal(graphed.x.cpu().numpy(), eager.x.cpu().numpy())
