@@ -85,6 +85,13 @@ int hx_repack_factors(const hx_plan* plan, const double* src, int64_t n_el, doub
 int hx_apply(const hx_plan* plan, const double* q, const double* factors, double* out,
              int64_t n_el, int* status_flag, void* stream);
 
+/* hx_apply on the element range [e_begin, e_end) of full-size arrays (q, out:
+ * n_el * (degree+1)^3 doubles from element 0; factors from element 0): the
+ * range form of SURVEY.md §8b's boundary, what a rank of the element
+ * partition calls (operators.py:324-331 chunks the same way).              */
+int hx_apply_range(const hx_plan* plan, const double* q, const double* factors, double* out,
+                   int64_t e_begin, int64_t e_end, int* status_flag, void* stream);
+
 /* End-to-end variant on HOST q / out (page-locked for full overlap): chunks of
  * up to `chunk_el` elements (ramped up and down at the ends) are copied in,
  * applied and copied back on a three-stream pipeline with three buffer slots,

@@ -177,6 +177,16 @@ int hx_apply(const hx_plan* P, const double* q, const double* factors, double* o
   return cuda_status(launch(*P, q, factors, out, n_el, flag, static_cast<cudaStream_t>(stream)));
 }
 
+int hx_apply_range(const hx_plan* P, const double* q, const double* factors, double* out,
+                   int64_t e_begin, int64_t e_end, int* flag, void* stream) {
+  if (!P || e_begin < 0 || e_end < e_begin) return HX_EINVAL;
+  const int64_t n3 = int64_t(P->n) * P->n * P->n;
+  if (e_end == e_begin) return HX_OK;
+  if (!q || !factors || !out) return HX_EINVAL;
+  return hx_apply(P, q + e_begin * n3, factors + e_begin * P->elem_stride, out + e_begin * n3,
+                  e_end - e_begin, flag, stream);
+}
+
 int64_t hx_apply_baseline_workspace(const hx_plan* P, int64_t n_el) {
   if (!P || n_el < 0) return -1;
   return baseline_workspace_doubles(*P, n_el) * int64_t(sizeof(double));

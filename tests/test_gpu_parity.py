@@ -278,3 +278,24 @@ def test_unfused_baseline_path_matches_oracle(bp, deg, mesh3):
     op1 = hx.make_operator(bp, deg, sub_mesh(mesh3, 1), lam=0.7)
     with pytest.raises(ValueError):
         hx.apply_baseline(op1, bad)
+
+
+@pytest.mark.parametrize("bp", BPS)
+def test_apply_range_over_partition_bitwise(bp, mesh3):
+    """hx_apply_range over the reference chunking's ranges (operators.py:324)
+    fills the full output bit for bit like one hx_apply."""
+    from paper_1711_00903_b200.shard import partition
+
+    op = hx.make_operator(bp, 7, mesh3, lam=0.3)
+    q = torch.from_numpy(np.random.default_rng(4).standard_normal((27, op.n_p))).cuda()
+    full = torch.empty_like(q)
+    hx.apply_device(op, q, full)
+    out = torch.full_like(q, float("nan"))
+    L = _native.lib()
+    for lo, hi in partition(27, 4):
+        _native.check(L.hx_apply_range(op.plan.handle, _native.ptr(q),
+                                       _native.ptr(op.device_factors), _native.ptr(out), lo, hi,
+                                       None, None))
+    np.testing.assert_array_equal(out.cpu().numpy(), full.cpu().numpy())
+    assert L.hx_apply_range(op.plan.handle, _native.ptr(q), _native.ptr(op.device_factors),
+                            _native.ptr(out), 5, 4, None, None) == _native.HX_EINVAL
