@@ -53,3 +53,27 @@ def test_reference_arm_contract():
     d = _run("--impl", "reference", "--steps", "1", "--warmup", "3")
     assert d["impl"] == "reference" and d["value"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["value"] == d["value"]
+
+
+def test_bench_two_ranks_weak_scaling_line():
+    """The N>1 path of bench.py (torchrun, barrier, max-over-ranks time,
+    summed DOFs, rank-0 line) with two ranks sharing the one GPU over gloo
+    (NCCL needs one GPU per rank; the driver's multi-GPU runs use it)."""
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    env = dict(os.environ, HX_BENCH_BACKEND="gloo")
+    res = subprocess.run(
+        [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+         "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+         "--gpus", "2", "--quick", "--steps", "3", "--warmup", "3"],
+        capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    assert res.returncode == 0, res.stderr[-3000:]
+    lines = [line for line in res.stdout.splitlines() if line.startswith("{")]
+    assert len(lines) == 1, res.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "weak" and d["value"] > 0
+    assert "x2" in d["config"]["parallelism"]
