@@ -40,10 +40,10 @@ def up_to_date():
     return all(os.path.getmtime(d) <= t for d in _deps())
 
 
-def _compile(src, defines=(), build_dir=BUILD):
+def _compile(src, defines=(), build_dir=BUILD, extra=()):
     obj = os.path.join(build_dir, os.path.basename(src) + ".o")
     log = obj + ".ptxas.log"
-    cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-c", src, "-o", obj]
+    cmd = [NVCC, *ARCH, *FLAGS, *extra, *[f"-D{d}" for d in defines], "-c", src, "-o", obj]
     res = subprocess.run(cmd, capture_output=True, text=True)
     with open(log, "w") as fh:
         fh.write(res.stdout + res.stderr)
@@ -52,21 +52,22 @@ def _compile(src, defines=(), build_dir=BUILD):
     return obj
 
 
-def build(force=False, verbose=False, defines=(), lib=LIB):
-    """Build the library (``defines``/``lib`` are for tuning experiments:
-    variant builds go to a separate path and never replace the product)."""
-    if not force and not defines and lib == LIB and up_to_date():
+def build(force=False, verbose=False, defines=(), lib=LIB, extra_flags=()):
+    """Build the library (``defines``/``lib``/``extra_flags`` are for tuning
+    experiments: variant builds go to a separate path and never replace the
+    product)."""
+    if not force and not defines and not extra_flags and lib == LIB and up_to_date():
         return LIB
-    if defines:
+    if defines or extra_flags:
         import hashlib
-        tag = hashlib.sha1("|".join(defines).encode()).hexdigest()[:12]
+        tag = hashlib.sha1("|".join((*defines, *extra_flags)).encode()).hexdigest()[:12]
         build_dir = os.path.join(BUILD, "v_" + tag)
     else:
         build_dir = BUILD
     os.makedirs(build_dir, exist_ok=True)
     srcs = _sources()
     with ThreadPoolExecutor(max_workers=min(len(srcs), os.cpu_count() or 4)) as pool:
-        objs = list(pool.map(lambda s: _compile(s, defines, build_dir), srcs))
+        objs = list(pool.map(lambda s: _compile(s, defines, build_dir, extra_flags), srcs))
     tmp = lib + ".tmp"
     cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart_static", "-lrt", "-ldl",
            "-lpthread"]
