@@ -18,6 +18,10 @@
  *   - every call that takes a `stream` is asynchronous on that cudaStream_t
  *     (NULL = legacy default stream) and never synchronises the device.
  *   - status: 0 on success, otherwise an HX_E* code; hx_strerror explains it.
+ *   - threads: a plan is immutable after hx_plan_create, so calls on one plan
+ *     from several host threads / streams are safe for distinct outputs; the
+ *     host-buffer pipeline's lazily created streams are the one shared
+ *     resource and hx_apply_host serialises its enqueue per plan.
  */
 #ifndef HEXBENCH_B200_H
 #define HEXBENCH_B200_H

@@ -253,6 +253,7 @@ int hx_apply_host(const hx_plan* Pc, const double* q_host, const double* factors
   if (n_el == 0) return HX_OK;
   if (!q_host || !factors || !out_host || !work) return HX_EINVAL;
   hx_plan* P = const_cast<hx_plan*>(Pc);  // lazily owned pipeline resources
+  std::lock_guard<std::mutex> lock(P->pipe_mu);
   cudaStream_t caller = static_cast<cudaStream_t>(stream);
   cudaError_t err;
   if (!P->pipe_ready) {

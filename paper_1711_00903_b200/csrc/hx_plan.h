@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cstdint>
+#include <mutex>
 #include <cuda_runtime.h>
 
 #include "../../include/hexbench_b200.h"
@@ -29,10 +30,13 @@ struct hx_plan {
   int n_slots;            // factor slots kept on device (1 for BP1, 7 otherwise)
   int64_t slot_stride;    // doubles per slot (q^3 rounded up to even)
   int64_t elem_stride;    // doubles per element (n_slots * slot_stride)
-  // lazily created resources for the host-buffer (end-to-end) path
+  // lazily created resources for the host-buffer (end-to-end) path; `pipe_mu`
+  // serialises hx_apply_host calls on one plan (they share these streams and
+  // events), everything else about a plan is immutable after create
   cudaStream_t pipe[3];
   cudaEvent_t ev[3][hx_host_slots];
   bool pipe_ready;
+  std::mutex pipe_mu;
 };
 
 namespace hx {
