@@ -299,3 +299,33 @@ def test_apply_range_over_partition_bitwise(bp, mesh3):
     np.testing.assert_array_equal(out.cpu().numpy(), full.cpu().numpy())
     assert L.hx_apply_range(op.plan.handle, _native.ptr(q), _native.ptr(op.device_factors),
                             _native.ptr(out), 5, 4, None, None) == _native.HX_EINVAL
+
+
+def test_host_path_concurrent_threads_on_one_plan(mesh3):
+    """Two host threads driving hx_apply_host on the same plan at once
+    (ctypes drops the GIL): the shared pipeline is serialised per plan and
+    both results are exact."""
+    import threading
+
+    op = hx.make_operator(hx.BP35, 5, mesh3, lam=0.5)
+    qs = [np.random.default_rng(s).standard_normal((27, op.n_p)) for s in (1, 2)]
+    want = [dev_apply(op, q) for q in qs]
+    outs = [np.empty_like(q) for q in qs]
+    errors = []
+
+    def work(i):
+        try:
+            for _ in range(20):
+                hx.apply_host(op, qs[i], outs[i], chunk_el=4)
+                torch.cuda.synchronize()
+        except Exception as exc:  # pragma: no cover - reported below
+            errors.append(exc)
+
+    threads = [threading.Thread(target=work, args=(i,)) for i in range(2)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    for got, ref in zip(outs, want):
+        np.testing.assert_array_equal(got, ref)
