@@ -26,29 +26,6 @@
 #define HX_MINB_BP1_OF(N) Cfg<kBP1, N>::MINB
 #endif
 
-// HX_BP1_XDB: double-buffer X across tiles so the end-of-tile barrier goes
-// (a tile's S1 writes the buffer the previous tile's S5 is not reading), and
-// warps that finish S5 start the next tile's loads while others still store.
-// Measured 2-3 % slower at N=7 and most other N (exp10): off.
-#ifndef HX_BP1_XDB
-#define HX_BP1_XDB 0
-#endif
-
-#ifndef HX_BP1_SPLIT_FULL
-#define HX_BP1_SPLIT_FULL 0
-#endif
-
-// HX_BP1_SHARED_FOLD: apply I^T from I's own fold (fold_apply_T) instead of
-// a second coefficient set, so S3's I_t and I_t^T read the same constants.
-#ifndef HX_BP1_SHARED_FOLD
-#define HX_BP1_SHARED_FOLD 0
-#endif
-#if HX_BP1_SHARED_FOLD
-#define HX_BP1_PROJECT(in, out) fold_apply_T<m, n>(p.I, in, out)
-#else
-#define HX_BP1_PROJECT(in, out) fold_apply<n, m, 1>(p.It, in, out)
-#endif
-
 namespace hx {
 
 template <int N>
@@ -87,9 +64,8 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT, HX_MINB_BP1_OF(N))
   extern __shared__ double smem[];
   uint64_t* const qbar = reinterpret_cast<uint64_t*>(smem);
   double* const QT = smem + (QST ? 2 : 0);
-  constexpr bool XDB = HX_BP1_XDB != 0;
   double* const X = QT + (QST ? EPB * n * QS : 0);
-  double* const Y = X + EPB * EX * (XDB ? 2 : 1);
+  double* const Y = X + EPB * EX;
 
   const int tid = threadIdx.x;
   const int64_t ntiles = (p.n_el + EPB - 1) / EPB;
@@ -124,13 +100,9 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT, HX_MINB_BP1_OF(N))
   }
 
   double en = 0.0;  // this thread's share of <q, A q> (ENERGY)
-  int parity = 0;   // which X buffer this tile uses (XDB)
-  // The tile body takes the tile's element count; full tiles (all but the
-  // last) pass the compile-time EPB so the per-line `el >= ne` guards fold
-  // away (HX_BP1_SPLIT_FULL).
-  auto tile_body = [&](const int64_t tile, const int ne) __attribute__((always_inline)) {
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t e0 = tile * EPB;
-    double* const Xt = X + (XDB && parity ? EPB * EX : 0);
+    const int ne = int(min64(EPB, p.n_el - e0));
     if (tid == 0) {
       const int64_t nt = tile + gridDim.x;
       if (nt < ntiles) {
@@ -168,7 +140,7 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT, HX_MINB_BP1_OF(N))
       const bool bad = any_nonfinite(x);
       if (bad && p.flag) atomicOr(p.flag, 1);
       fold_apply<m, n, 1>(p.I, x, y);
-      double* dst = Xt + el * EX + LX.kofs(k) + i;
+      double* dst = X + el * EX + LX.kofs(k) + i;
 #pragma unroll
       for (int t = 0; t < m; ++t) dst[t * LX.s1] = y[t];
     });
@@ -186,7 +158,7 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT, HX_MINB_BP1_OF(N))
       if (el >= ne) return;
       int k, a;
       iline_coords<n, m, IORD>(ln, k, a);
-      const double* src = Xt + el * EX + LX.kofs(k) + a * LX.s1;
+      const double* src = X + el * EX + LX.kofs(k) + a * LX.s1;
       double x[n], y[m];
 #pragma unroll
       for (int t = 0; t < n; ++t) x[t] = src[t];
@@ -221,7 +193,7 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT, HX_MINB_BP1_OF(N))
         if constexpr (ENERGY) en += wy * y[t];  // <q, A q> = sum GwJ (I q)^2
         y[t] = wy;
       }
-      HX_BP1_PROJECT(y, x);
+      fold_apply<n, m, 1>(p.It, y, x);
 #pragma unroll
       for (int t = 0; t < n; ++t) line[LY.kofs(t)] = x[t];
     });
@@ -236,8 +208,8 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT, HX_MINB_BP1_OF(N))
       double x[m], y[n];
 #pragma unroll
       for (int t = 0; t < m; ++t) x[t] = src[t];
-      HX_BP1_PROJECT(x, y);
-      double* dst = Xt + el * EX + LX.kofs(k) + a * LX.s1;
+      fold_apply<n, m, 1>(p.It, x, y);
+      double* dst = X + el * EX + LX.kofs(k) + a * LX.s1;
 #pragma unroll
       for (int t = 0; t < n; ++t) dst[t] = y[t];
     });
@@ -248,23 +220,16 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT, HX_MINB_BP1_OF(N))
       if (el >= ne) return;
       int k, i;
       line_coords<n, n, JKF>(ln, k, i);
-      const double* src = Xt + el * EX + LX.kofs(k) + i;
+      const double* src = X + el * EX + LX.kofs(k) + i;
       double x[m], y[n];
 #pragma unroll
       for (int t = 0; t < m; ++t) x[t] = src[t * LX.s1];
-      HX_BP1_PROJECT(x, y);
+      fold_apply<n, m, 1>(p.It, x, y);
       double* dst = p.out + (e0 + el) * n3 + k * n2 + i;
 #pragma unroll
       for (int t = 0; t < n; ++t) st_stream(dst + t * n, y[t]);
     });
-    if constexpr (!XDB) __syncthreads();  // X is rewritten by the next tile's S1
-  };
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, parity ^= 1) {
-    const int ne = int(min64(EPB, p.n_el - tile * EPB));
-    if (HX_BP1_SPLIT_FULL && ne == EPB)
-      tile_body(tile, EPB);
-    else
-      tile_body(tile, ne);
+    __syncthreads();  // X is rewritten by the next tile's S1
   }
   if constexpr (ENERGY) {
     const double sum = block_sum<C::NT>(en, X);

@@ -35,13 +35,6 @@
 #ifndef HX_BP3_REREAD_MIN_N
 #define HX_BP3_REREAD_MIN_N 7
 #endif
-// S5 stalls on its factor loads (L2 hits after the bulk prefetch, but with
-// 16 warps per SM the latency is exposed: r12 ncu, 38 % of stall samples).
-// The first HX_BP3_FPF t-slices of this thread's factors are therefore
-// loaded into registers at the end of S4, before the barrier.
-#ifndef HX_BP3_FPF
-#define HX_BP3_FPF 0
-#endif
 #ifndef HX_PF_BP3
 #define HX_PF_BP3 2  // stage at which a tile's factors are prefetched into L2
 #endif
@@ -170,8 +163,6 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT, HX_MINB_BP3_OF(N))
     __syncthreads();
     // ---- S4: r- and s-derivatives of T
     if (HX_PF_BP3 == 4 && tid == 0) prefetch_l2(p.fac + e0 * fs, ne * fs * sizeof(double));
-    constexpr int FPF = HX_BP3_FPF < m ? HX_BP3_FPF : m;
-    double gpf[FPF > 0 ? FPF : 1][7];  // factors of S5's first FPF t-slices
     if (act_c) {
       const int kk = ln_c / m, r = ln_c % m;
       double x[m], y[m];
@@ -189,11 +180,6 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT, HX_MINB_BP3_OF(N))
       dst = Bc + LQS.kofs(kk) + r;
 #pragma unroll
       for (int t = 0; t < m; ++t) dst[t * LQS.s1] = y[t];
-      const double* gp = p.fac + (e0 + el_c) * fs + ln_c;
-#pragma unroll
-      for (int t = 0; t < FPF; ++t)
-#pragma unroll
-        for (int sl = 0; sl < 7; ++sl) gpf[t][sl] = gp[t * m2 + sl * ss];
     }
     __syncthreads();
     // ---- S5: chain rule on k-lines (a, c)
@@ -218,14 +204,9 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT, HX_MINB_BP3_OF(N))
 #pragma unroll
       for (int t = 0; t < m; ++t) {
         const double* gk = g + t * m2;
-        const bool pre = t < FPF;
-        const double grr = pre ? gpf[t < FPF ? t : 0][0] : gk[0];
-        const double grs = pre ? gpf[t < FPF ? t : 0][1] : gk[ss];
-        const double grt = pre ? gpf[t < FPF ? t : 0][2] : gk[2 * ss];
-        const double gss = pre ? gpf[t < FPF ? t : 0][3] : gk[3 * ss];
-        const double gst = pre ? gpf[t < FPF ? t : 0][4] : gk[4 * ss];
-        const double gtt = pre ? gpf[t < FPF ? t : 0][5] : gk[5 * ss];
-        const double gwj = pre ? gpf[t < FPF ? t : 0][6] : gk[6 * ss];
+        const double grr = gk[0], grs = gk[ss], grt = gk[2 * ss];
+        const double gss = gk[3 * ss], gst = gk[4 * ss], gtt = gk[5 * ss];
+        const double gwj = gk[6 * ss];
         const double qr = qrl[LQR.kofs(t)], qs = qsl[LQS.kofs(t)], qt = tt[t];
         const double rqr = grr * qr + grs * qs + grt * qt;
         const double rqs = grs * qr + gss * qs + gst * qt;

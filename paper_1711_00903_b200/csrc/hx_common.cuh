@@ -79,43 +79,6 @@ __device__ __forceinline__ void fold_apply(const Fold<R, C>& F, const double (&x
   }
 }
 
-// y = M^T x for a folded CENTRO-SYMMETRIC R x C matrix M, from M's own fold:
-// the fold of M^T is the transpose of M's (e'[b][a] = e[a][b], o'[b][a] =
-// o[a][b] -- centro-symmetry maps M[R-1-a][b] to M[a][C-1-b]), so a kernel
-// applying both I and I^T needs only I's coefficients.
-template <int R, int C>
-__device__ __forceinline__ void fold_apply_T(const Fold<R, C>& F, const double (&x)[R],
-                                             double (&y)[C]) {
-  constexpr int HI = R / 2, HO = C / 2;  // of M^T: input pairs, output pairs
-  constexpr bool MID_IN = R & 1, MID_OUT = C & 1;
-  double xe[HI], xo[HI];
-#pragma unroll
-  for (int a = 0; a < HI; ++a) {
-    xe[a] = x[a] + x[R - 1 - a];
-    xo[a] = x[a] - x[R - 1 - a];
-  }
-#pragma unroll
-  for (int b = 0; b < HO; ++b) {
-    double ye = F.e[0][b] * xe[0];
-    double yo = F.o[0][b] * xo[0];
-#pragma unroll
-    for (int a = 1; a < HI; ++a) {
-      ye = fma(F.e[a][b], xe[a], ye);
-      yo = fma(F.o[a][b], xo[a], yo);
-    }
-    if constexpr (MID_IN) ye = fma(F.e[HI][b], x[HI], ye);
-    y[b] = ye + yo;
-    y[C - 1 - b] = ye - yo;
-  }
-  if constexpr (MID_OUT) {
-    double ye = F.e[0][HO] * xe[0];
-#pragma unroll
-    for (int a = 1; a < HI; ++a) ye = fma(F.e[a][HO], xe[a], ye);
-    if constexpr (MID_IN) ye = fma(F.e[HI][HO], x[HI], ye);
-    y[HO] = ye;
-  }
-}
-
 // Host: fill a Fold from a dense row-major R x C matrix.
 template <int R, int C>
 inline void fill_fold(Fold<R, C>& F, const double* M) {
@@ -323,10 +286,6 @@ constexpr int smem_doubles() {
   for (int b = 0; b < int(sizeof(C::EBUF) / sizeof(int)); ++b) s += C::EBUF[b];
   s *= C::EPB;
   if (C::QS > 0) s += 2 + C::EPB * (N + 1) * C::QS;
-#ifndef HX_BP1_XDB
-#define HX_BP1_XDB 0
-#endif
-  if (BP == kBP1 && HX_BP1_XDB) s += C::EPB * C::EBUF[0];  // second X buffer (hx_bp1.cu)
   return s;
 }
 
