@@ -63,12 +63,16 @@ class CGWorkspace:
         self.pap = torch.zeros(1, dtype=torch.float64, device=like.device)
 
 
-def cg_solve(op, b, x0=None, tol=1e-10, maxiter=500, check_every=10, group=None, work=None):
+def cg_solve(op, b, x0=None, tol=1e-10, maxiter=500, check_every=10, group=None, work=None,
+             graph=False):
     """Solve A x = b for a device-resident right-hand side.
 
     ``op`` is an OperatorInstance (or this rank's ShardedOperator.op); ``b`` a
     float64 CUDA tensor of shape (op.n_el, op.n_p).  Converged when
     ||r|| <= tol * ||b|| (checked every ``check_every`` iterations).
+    ``graph=True`` (single process): the iterations between two checks run as
+    one captured CUDA graph (see AssembledCG); same iterates bit for bit, the
+    iteration count rounded up to whole blocks.
     """
     import torch
 
@@ -101,25 +105,55 @@ def cg_solve(op, b, x0=None, tol=1e-10, maxiter=500, check_every=10, group=None,
         return CGResult(x, 0, True, norms)
     it = 0
     converged = False
-    while it < maxiter:
-        nxt = 1 - cur
+
+    def step(c, strm):
+        nx = 1 - c
         _native.check(L.hx_apply_energy(op.plan.handle, ptr(w.p), ptr(op.device_factors),
                                         ptr(w.ap), op.n_el, ptr(w.partials), w.npart,
-                                        ptr(w.pap), ptr(flag), stream), "hx_apply_energy")
+                                        ptr(w.pap), ptr(flag), strm), "hx_apply_energy")
         _allreduce(w.pap, group)
-        _native.check(L.hx_cg_update(ptr(x), ptr(w.p), ptr(w.r), ptr(w.ap), n, ptr(w.rr[cur]),
-                                     ptr(w.pap), ptr(w.partials), w.npart, ptr(w.rr[nxt]),
-                                     stream), "hx_cg_update")
-        _allreduce(w.rr[nxt], group)
-        it += 1
-        if it % check_every == 0 or it == maxiter:
-            norms.append(float(w.rr[nxt].sqrt().item()))
+        _native.check(L.hx_cg_update(ptr(x), ptr(w.p), ptr(w.r), ptr(w.ap), n, ptr(w.rr[c]),
+                                     ptr(w.pap), ptr(w.partials), w.npart, ptr(w.rr[nx]),
+                                     strm), "hx_cg_update")
+        _allreduce(w.rr[nx], group)
+        return nx
+
+    def direction(c, nx, strm):
+        _native.check(L.hx_cg_direction(ptr(w.p), ptr(w.r), n, ptr(w.rr[nx]), ptr(w.rr[c]),
+                                        strm), "hx_cg_direction")
+
+    import torch.distributed as dist
+    if graph and not (dist.is_available() and dist.is_initialized()):
+        k = check_every + (check_every % 2)
+
+        def block():
+            c, strm = 0, _stream(dev)
+            for _ in range(k):
+                nx = step(c, strm)
+                direction(c, nx, strm)
+                c = nx
+
+        run = block  # first block eager (first-launch setup), then captured
+        while it < maxiter:
+            run()
+            it += k
+            norms.append(float(w.rr[0].sqrt().item()))
             if norms[-1] <= target:
                 converged = True
                 break
-        _native.check(L.hx_cg_direction(ptr(w.p), ptr(w.r), n, ptr(w.rr[nxt]), ptr(w.rr[cur]),
-                                        stream), "hx_cg_direction")
-        cur = nxt
+            if run is block:
+                run = _graphed(block)
+    else:
+        while it < maxiter:
+            nxt = step(cur, stream)
+            it += 1
+            if it % check_every == 0 or it == maxiter:
+                norms.append(float(w.rr[nxt].sqrt().item()))
+                if norms[-1] <= target:
+                    converged = True
+                    break
+            direction(cur, nxt, stream)
+            cur = nxt
     if int(flag.item()) & _native.HX_FLAG_NONFINITE:
         raise ValueError("non-finite values during the CG solve")
     return CGResult(x, it, converged, norms)

@@ -132,3 +132,14 @@ def test_report_cli_json_and_csv(tmp_path):
     assert rows[0] == ["bp", "N", "F", "bytes", "R_global", "R_shared"]
     assert [int(r[1]) for r in rows[1:]] == [1, 2, 3]
     assert all(float(r[4]) > 0 and float(r[5]) > 0 for r in rows[1:])
+
+
+def test_graphed_element_local_cg_bitwise(mesh3):
+    from paper_1711_00903_b200.cg import cg_solve
+
+    op = hx.make_operator(hx.BP3, 4, mesh3, lam=0.8)
+    b = torch.from_numpy(np.random.default_rng(6).standard_normal((27, op.n_p))).cuda()
+    eager = cg_solve(op, b, tol=1e-11, check_every=10)
+    graphed = cg_solve(op, b, tol=1e-11, check_every=10, graph=True)
+    assert eager.converged and graphed.converged and graphed.iterations == eager.iterations
+    np.testing.assert_array_equal(graphed.x.cpu().numpy(), eager.x.cpu().numpy())
