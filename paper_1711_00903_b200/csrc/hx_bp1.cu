@@ -237,173 +237,6 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT, HX_MINB_BP1_OF(N))
   }
 }
 
-// ---- slab-per-warp schedule (experiment, N=7, HX_BP1_SLAB) ----------------
-// The 24 k-slabs of a 3-element tile are owned by the 8 warps, 3 slabs each.
-// The slab-local stages (S1/S2: j- then i-interpolation, S4/S5: i- then
-// j-projection) then need only __syncwarp; CTA barriers remain around the
-// k-direction stage S3 alone (2 per tile instead of 5).  Lanes map to
-// (slab, line) through permutation tables chosen with the slab bases so that
-// every half-warp hits 16 distinct banks in S1/S5 (j-lines) and S2/S4
-// (i-lines) alike (bank offsets 0, 4, 10 of the warp's three slabs).
-#ifndef HX_BP1_SLAB
-#define HX_BP1_SLAB 0
-#endif
-
-namespace slab7 {
-constexpr int n = 8, m = 9;
-constexpr int BXW = 256, BYW = 288;          // per-warp X / Y blocks (doubles)
-// slab bases within a block: X 0, 84, 170 / Y 0, 100, 202 (both 0, 4, 10 mod 16)
-// j-line stages: lane -> j * 16 + i (j = slab within the warp), -1 idle
-__constant__ int T1[32] = {0, 1, 2, 3, 4, 5, 6, 7, 20, 21, 22, 23, 34, 35, 36, 37,
-                        38, 39, 16, 17, 18, 19, 32, 33, -1, -1, -1, -1, -1, -1, -1, -1};
-// i-line stages: lane -> j * 16 + a
-__constant__ int T2[32] = {0, 21, 2, 23, 4, 35, 6, 37, 8, 1, 22, 3, 24, 5, 36, 7,
-                        38, 40, 33, 16, 18, 20, 39, 32, 34, 17, 19, -1, -1, -1, -1, -1};
-__device__ __forceinline__ int xbase(int g) {
-  const int j = g % 3;
-  return (g / 3) * BXW + (j == 0 ? 0 : (j == 1 ? 84 : 170));
-}
-__device__ __forceinline__ int ybase(int g) {
-  const int j = g % 3;
-  return (g / 3) * BYW + (j == 0 ? 0 : (j == 1 ? 100 : 202));
-}
-}  // namespace slab7
-
-template <bool ENERGY>
-__global__ void __launch_bounds__(256, 4)
-    bp1_slab7_kernel(const __grid_constant__ BP1Params<7> p) {
-  using namespace slab7;
-  constexpr int EPB = 3, NT = 256, n2 = n * n, n3 = n2 * n, m2 = m * m;
-  extern __shared__ double smem[];
-  double* const X = smem;
-  double* const Y = smem + 8 * BXW;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t ntiles = (p.n_el + EPB - 1) / EPB;
-  const int64_t fs = p.fac_estride;
-  const int c1 = T1[lane], c2 = T2[lane];
-  const int g1 = 3 * warp + (c1 >> 4), i1 = c1 & 15;  // S1/S5 slab and i
-  const int g2 = 3 * warp + (c2 >> 4), a2 = c2 & 15;  // S2/S4 slab and a
-  if (tid == 0 && blockIdx.x < ntiles) {
-    const int64_t e0 = int64_t(blockIdx.x) * EPB;
-    const int64_t ne = min64(EPB, p.n_el - e0);
-    prefetch_l2(p.q + e0 * n3, ne * n3 * sizeof(double));
-    prefetch_l2(p.gwj + e0 * fs, ne * fs * sizeof(double));
-  }
-  double en = 0.0;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t e0 = tile * EPB;
-    const int ne = int(min64(EPB, p.n_el - e0));
-    if (tid == 0) {
-      const int64_t nt = tile + gridDim.x;
-      if (nt < ntiles) {
-        const int64_t f0 = nt * EPB;
-        const int64_t nn = min64(EPB, p.n_el - f0);
-        prefetch_l2(p.q + f0 * n3, nn * n3 * sizeof(double));
-        prefetch_l2(p.gwj + f0 * fs, nn * fs * sizeof(double));
-      }
-    }
-    // S3's GwJ k-line, loaded early
-    double w[m];
-    const int el_c = tid / m2, ln_c = tid % m2;
-    if (el_c < ne) {
-      const double* gp = p.gwj + (e0 + el_c) * fs + ln_c;
-#pragma unroll
-      for (int c = 0; c < m; ++c) w[c] = gp[c * m2];
-    }
-    // ---- S1: j-lines of the warp's slabs -> X rows
-    if (c1 >= 0 && g1 / n < ne) {
-      const int el = g1 / n, k = g1 % n;
-      const double* src = p.q + (e0 + el) * n3 + k * n2 + i1;
-      double x[n], y[m];
-#pragma unroll
-      for (int t = 0; t < n; ++t) x[t] = src[t * n];
-      if (any_nonfinite(x) && p.flag) atomicOr(p.flag, 1);
-      fold_apply<m, n, 1>(p.I, x, y);
-      double* dst = X + xbase(g1) + i1;
-#pragma unroll
-      for (int t = 0; t < m; ++t) dst[t * 9] = y[t];
-    }
-    __syncwarp();
-    // ---- S2: i-lines (k, a) -> Y rows
-    if (c2 >= 0 && g2 / n < ne) {
-      const double* src = X + xbase(g2) + a2 * 9;
-      double x[n], y[m];
-#pragma unroll
-      for (int t = 0; t < n; ++t) x[t] = src[t];
-      fold_apply<m, n, 1>(p.I, x, y);
-      double* dst = Y + ybase(g2) + a2 * 9;
-#pragma unroll
-      for (int t = 0; t < m; ++t) dst[t] = y[t];
-    }
-    __syncthreads();
-    // ---- S3: k-lines (a, c) across the element's 8 slabs
-    if (el_c < ne) {
-      double x[n], y[m];
-#pragma unroll
-      for (int t = 0; t < n; ++t) x[t] = Y[ybase(el_c * n + t) + ln_c];
-      fold_apply<m, n, 1>(p.I, x, y);
-#pragma unroll
-      for (int t = 0; t < m; ++t) {
-        const double wy = y[t] * w[t];
-        if constexpr (ENERGY) en += wy * y[t];
-        y[t] = wy;
-      }
-      fold_apply<n, m, 1>(p.It, y, x);
-#pragma unroll
-      for (int t = 0; t < n; ++t) Y[ybase(el_c * n + t) + ln_c] = x[t];
-    }
-    __syncthreads();
-    // ---- S4: i-lines: Y rows -> X rows (projected along r)
-    if (c2 >= 0 && g2 / n < ne) {
-      const double* src = Y + ybase(g2) + a2 * 9;
-      double x[m], y[n];
-#pragma unroll
-      for (int t = 0; t < m; ++t) x[t] = src[t];
-      fold_apply<n, m, 1>(p.It, x, y);
-      double* dst = X + xbase(g2) + a2 * 9;
-#pragma unroll
-      for (int t = 0; t < n; ++t) dst[t] = y[t];
-    }
-    __syncwarp();
-    // ---- S5: j-lines -> out
-    if (c1 >= 0 && g1 / n < ne) {
-      const int el = g1 / n, k = g1 % n;
-      const double* src = X + xbase(g1) + i1;
-      double x[m], y[n];
-#pragma unroll
-      for (int t = 0; t < m; ++t) x[t] = src[t * 9];
-      fold_apply<n, m, 1>(p.It, x, y);
-      double* dst = p.out + (e0 + el) * n3 + k * n2 + i1;
-#pragma unroll
-      for (int t = 0; t < n; ++t) st_stream(dst + t * n, y[t]);
-    }
-    __syncwarp();  // the next tile's S1 rewrites this warp's X rows
-  }
-  if constexpr (ENERGY) {
-    const double sum = block_sum<NT>(en, X);
-    if (tid == 0) p.energy[blockIdx.x] = sum;
-  }
-}
-
-template <bool E>
-static cudaError_t launch_slab7(const BP1Params<7>& prm, int64_t n_el, cudaStream_t s) {
-  constexpr int smem = (8 * slab7::BXW + 8 * slab7::BYW) * int(sizeof(double));
-  static int blocks_per_sm = -1;
-  if (blocks_per_sm < 0) {
-    cudaError_t err = cudaFuncSetAttribute(bp1_slab7_kernel<E>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (err != cudaSuccess) return err;
-    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, bp1_slab7_kernel<E>, 256,
-                                                        smem);
-    if (err != cudaSuccess) return err;
-    if (blocks_per_sm < 1) blocks_per_sm = 1;
-  }
-  const int64_t ntiles = (n_el + 2) / 3;
-  const int64_t grid = min64(ntiles, int64_t(blocks_per_sm) * sm_count());
-  bp1_slab7_kernel<E><<<unsigned(grid), 256, smem, s>>>(prm);
-  return cudaGetLastError();
-}
-
 template <int N, bool E, bool STAGE, class Prm>
 static cudaError_t launch_t(const Prm& prm, int64_t n_el, cudaStream_t s) {
   using C = Cfg<kBP1, N>;
@@ -452,8 +285,6 @@ static cudaError_t launch_n(const hx_plan& P, const double* q, const double* fac
   prm.fac_estride = P.elem_stride;
   prm.flag = flag;
   prm.energy = energy;
-  if constexpr (N == 7 && HX_BP1_SLAB)
-    return energy ? launch_slab7<true>(prm, n_el, s) : launch_slab7<false>(prm, n_el, s);
   return energy ? launch_s<N, true>(prm, n_el, s) : launch_s<N, false>(prm, n_el, s);
 }
 
