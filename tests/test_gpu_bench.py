@@ -77,3 +77,27 @@ def test_bench_two_ranks_weak_scaling_line():
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["scaling"] == "weak" and d["value"] > 0
     assert "x2" in d["config"]["parallelism"]
+
+
+def test_scaling_tool_two_ranks(tmp_path):
+    """tools/scaling.py (config 5) through its multi-rank path: strong and
+    weak modes on two ranks sharing the GPU over gloo, small meshes."""
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    out = tmp_path / "scaling.jsonl"
+    env = dict(os.environ, HX_BENCH_BACKEND="gloo")
+    res = subprocess.run(
+        [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+         "--master-addr", "127.0.0.1", "--master-port", str(port),
+         os.path.join(ROOT, "tools", "scaling.py"), "--strong-side", "8", "--weak-side", "6",
+         "--steps", "3", "--warmup", "3", "--out", str(out)],
+        capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    assert res.returncode == 0, res.stderr[-3000:]
+    recs = [json.loads(line) for line in out.read_text().splitlines()]
+    assert len(recs) == 6 and all(r["gpus"] == 2 and r["gdof_per_s"] > 0 for r in recs)
+    strong = [r for r in recs if r["mode"] == "strong"]
+    assert all(r["n_el_total"] == 512 and r["n_el_per_gpu_max"] == 256 for r in strong)

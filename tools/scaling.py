@@ -30,19 +30,20 @@ DEG = 7
 
 
 def max_over_ranks(v):
-    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dev = "cpu" if dist.is_initialized() and dist.get_backend() == "gloo" else "cuda"
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
     if dist.is_initialized():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
 
-def run(mode, bp, rank, world, steps, warmup):
+def run(mode, bp, rank, world, steps, warmup, strong_side=92, weak_side=46):
     if mode == "strong":
-        mesh = hx.perturb_mesh(hx.build_cube_mesh(92, 2.0), amplitude=0.15, seed=7)
+        mesh = hx.perturb_mesh(hx.build_cube_mesh(strong_side, 2.0), amplitude=0.15, seed=7)
         sh = ShardedOperator(bp, DEG, mesh, lam=1.0, rank=rank, world_size=world)
         op, total_el = sh.op, mesh.n_el
     else:
-        mesh = hx.perturb_mesh(hx.build_cube_mesh(46, 2.0), amplitude=0.15, seed=7 + rank)
+        mesh = hx.perturb_mesh(hx.build_cube_mesh(weak_side, 2.0), amplitude=0.15, seed=7 + rank)
         op, total_el = hx.make_operator(bp, DEG, mesh, lam=1.0), mesh.n_el * world
     q = torch.randn(op.n_el, op.n_p, dtype=torch.float64, device="cuda")
     out = torch.empty_like(q)
@@ -61,7 +62,12 @@ def run(mode, bp, rank, world, steps, warmup):
                                         op.n_el, _native.ptr(partials), npart,
                                         _native.ptr(energy), None, stream))
         if dist.is_initialized():
-            dist.all_reduce(energy)
+            if dist.get_backend() == "gloo":
+                h = energy.cpu()
+                dist.all_reduce(h)
+                energy.copy_(h)
+            else:
+                dist.all_reduce(energy)
 
     for _ in range(warmup):
         step()
@@ -80,7 +86,9 @@ def run(mode, bp, rank, world, steps, warmup):
     # the all-reduce alone (8 bytes), for the record
     torch.cuda._sleep(200_000)
     s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    part = torch.ones(1, dtype=torch.float64, device="cuda")
+    part = torch.ones(1, dtype=torch.float64,
+                      device="cpu" if dist.is_initialized() and dist.get_backend() == "gloo"
+                      else "cuda")
     s2.record()
     for _ in range(steps):
         if dist.is_initialized():
@@ -106,17 +114,24 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--modes", default="strong,weak")
     ap.add_argument("--out", default=None)
+    ap.add_argument("--strong-side", type=int, default=92)
+    ap.add_argument("--weak-side", type=int, default=46)
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1 or "MASTER_ADDR" in os.environ:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("HX_BENCH_BACKEND", "nccl")  # gloo: test-only, ranks share a GPU
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     fh = open(args.out, "a") if (args.out and rank == 0) else None
     for mode in args.modes.split(","):
         for bp in hx.BENCHMARKS:
-            rec = run(mode, bp, rank, world, args.steps, args.warmup)
+            rec = run(mode, bp, rank, world, args.steps, args.warmup, args.strong_side,
+                      args.weak_side)
             if rank == 0:
                 line = json.dumps(rec)
                 print(line, flush=True)
