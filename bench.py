@@ -200,11 +200,11 @@ def sum_over_ranks(value, world):
     return float(t.item())
 
 
-def build_operator(bp, side, rank, geometry="stored"):
+def build_operator(bp, side, rank):
     import paper_1711_00903_b200 as hx
 
     mesh = hx.perturb_mesh(hx.build_cube_mesh(side, 2.0), amplitude=0.15, seed=7 + rank)
-    op = hx.make_operator(bp, DEGREE, mesh, lam=LAM, geometry=geometry)
+    op = hx.make_operator(bp, DEGREE, mesh, lam=LAM)
     return mesh, op
 
 
@@ -268,20 +268,15 @@ def time_applies(op, q, out, steps, warmup, flush=None):
     return [s.elapsed_time(e) for s, e in times]
 
 
-def bp_report(bp, side, rank, steps, warmup, hbm_peak, geometry="stored"):
-    """One BP at one size.  geometry="on_the_fly" (BP1.0): GwJ recomputed from
-    the corners, so the algorithmic bytes are q + out + 192 B of corners per
-    element instead of Table 1's q + out + GwJ."""
+def bp_report(bp, side, rank, steps, warmup, hbm_peak):
     import torch
     import paper_1711_00903_b200 as hx
 
-    mesh, op = build_operator(bp, side, rank, geometry)
+    mesh, op = build_operator(bp, side, rank)
     q = hx.FieldVector.random(mesh.n_el, op.n_p, seed=0).to_device().data
     out = torch.empty_like(q)
     t = hx.traffic(bp, DEGREE, mesh.n_el)
     bytes_per_apply = t.bytes_per_element * mesh.n_el
-    if geometry == "on_the_fly":
-        bytes_per_apply = (2 * op.n_p * 8 + 24 * 8) * mesh.n_el
     flops = hx.flop_model(bp, "fused", DEGREE) * mesh.n_el
     l2_resident = bytes_per_apply < 256e6
     flush = torch.zeros(64 << 20, dtype=torch.float64, device="cuda") if l2_resident else None
@@ -301,7 +296,6 @@ def bp_report(bp, side, rank, steps, warmup, hbm_peak, geometry="stored"):
         "b_copy_same_size_best_gb_per_s": b_copy_best / 1e9,
         "frac_of_copy_same_size": bytes_per_apply / (med * 1e-3) / b_copy_mean,
         "l2": "flushed before every apply" if l2_resident else "inputs larger than L2",
-        "geometry": geometry,
         "threads": op.plan.threads, "elements_per_tile": op.plan.elements_per_tile,
         "smem_bytes": op.plan.smem_bytes,
     }
@@ -665,9 +659,6 @@ def run_ours(args):
         for xbp, xside in EXTRA:
             r = bp_report(xbp, xside, 0, args.steps, args.warmup, hbm_peak)
             per_bp[f"{xbp} E={r['n_el']}"] = r
-        for xside in (16, 32):  # BP1.0 with on-the-fly geometry (opt-in mode)
-            r = bp_report(hx.BP1, xside, 0, args.steps, args.warmup, hbm_peak, "on_the_fly")
-            per_bp[f"BP1.0 E={r['n_el']} on-the-fly geometry"] = r
         cpu = cpu_baseline()
 
     if rank == 0:

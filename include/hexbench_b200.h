@@ -89,16 +89,6 @@ int hx_repack_factors(const hx_plan* plan, const double* src, int64_t n_el, doub
 int hx_apply(const hx_plan* plan, const double* q, const double* factors, double* out,
              int64_t n_el, int* status_flag, void* stream);
 
-/* BP1.0 with on-the-fly geometry: as hx_apply, but GwJ is recomputed inside
- * the kernel from the element corners `vertices` ((n_el, 8, 3) doubles on the
- * device, reference corner order mesh.py:9) instead of read from stored
- * factors -- exact for the reference's trilinear hexahedra (mesh.py:77-98),
- * 192 bytes of corners per element instead of (N+2)^3 doubles of GwJ.  The
- * reference has no such mode (it always stores factors, operators.py:133);
- * the result equals hx_apply's up to rounding.  BP3.5 / BP3.0 plans: EINVAL. */
-int hx_apply_geom(const hx_plan* plan, const double* q, const double* vertices, double* out,
-                  int64_t n_el, int* status_flag, void* stream);
-
 /* hx_apply on the element range [e_begin, e_end) of full-size arrays (q, out:
  * n_el * (degree+1)^3 doubles from element 0; factors from element 0): the
  * range form of SURVEY.md §8b's boundary, what a rank of the element

@@ -32,7 +32,6 @@ SIGNATURES = {
     "hx_repack_factors": (_c.c_int, [_P, _P, _c.c_int64, _P, _c.c_int, _P]),
     "hx_apply": (_c.c_int, [_P, _P, _P, _P, _c.c_int64, _P, _P]),
     "hx_apply_range": (_c.c_int, [_P, _P, _P, _P, _c.c_int64, _c.c_int64, _P, _P]),
-    "hx_apply_geom": (_c.c_int, [_P, _P, _P, _P, _c.c_int64, _P, _P]),
     "hx_apply_host_workspace": (_c.c_int64, [_P, _c.c_int64]),
     "hx_apply_host": (_c.c_int, [_P, _P, _P, _P, _c.c_int64, _c.c_int64, _P, _P, _P]),
     "hx_plan_kernel_shape": (_c.c_int, [_P, _c.POINTER(_c.c_int), _c.POINTER(_c.c_int),

@@ -39,59 +39,9 @@ struct BP1Params {
   int64_t fac_estride;
   int* flag;
   double* energy;  // per-CTA partials of <q, A q> (ENERGY instantiation only)
-  // GEOM instantiation: GwJ recomputed from the element corners
-  const double* verts;  // (n_el, 8, 3), reference corner order (mesh.py:9)
-  double xg[N + 2];     // GL nodes and weights of the factor rule
-  double wg[N + 2];
 };
 
-// On-the-fly geometry (GEOM): the trilinear map's Jacobian columns are
-//   dx/dr = A0 + s A1 + t A2 + s t A3,   dx/ds = B0 + r A1 + t B2 + r t A3,
-//   dx/dt = C0 + r A2 + s B2 + r s A3
-// with seven corner combinations per element (kc below, reference
-// mesh.py:77-90).  Along one k-line (r, s fixed) dx/dt is constant and the
-// other two columns are affine in t, so det(J) = d0 + t (d1 + t d2): GwJ at
-// the line's 9 points costs ~60 FP64 operations per line instead of 9 loads
-// of stored factors -- 192 bytes of corners per element replace 5.8 KB of GwJ
-// (BP1.0's traffic drops from 14,024 to 8,384 bytes per element at N=7).
-constexpr int kKC = 21;  // A0, A1, A2, A3, B0, B2, C0 (x, y, z each)
-
-__device__ __forceinline__ double corner_combo(const double* v, int vec, int comp) {
-  double acc = 0.0;
-#pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    const double r = (c & 4) ? 1.0 : -1.0, s = (c & 2) ? 1.0 : -1.0, t = (c & 1) ? 1.0 : -1.0;
-    const double sign = vec == 0 ? r : vec == 1 ? r * s : vec == 2 ? r * t : vec == 3 ? r * s * t
-                        : vec == 4 ? s : vec == 5 ? s * t : t;
-    acc = fma(sign, v[c * 3 + comp], acc);
-  }
-  return 0.125 * acc;
-}
-
-// det(J) along the k-line (r = xg[c], s = xg[a]) as d0 + t (d1 + t d2)
-__device__ __forceinline__ void line_det(const double* kc, double r, double s, double& d0,
-                                         double& d1, double& d2) {
-  double P[3], Q[3], R[3], S[3], T[3];
-#pragma unroll
-  for (int i = 0; i < 3; ++i) {
-    const double A0 = kc[i], A1 = kc[3 + i], A2 = kc[6 + i], A3 = kc[9 + i];
-    const double B0 = kc[12 + i], B2 = kc[15 + i], C0 = kc[18 + i];
-    P[i] = fma(s, A1, A0);
-    Q[i] = fma(s, A3, A2);
-    R[i] = fma(r, A1, B0);
-    S[i] = fma(r, A3, B2);
-    T[i] = fma(r * s, A3, fma(s, B2, fma(r, A2, C0)));
-  }
-  const double U0 = R[1] * T[2] - R[2] * T[1], U1 = R[2] * T[0] - R[0] * T[2],
-               U2 = R[0] * T[1] - R[1] * T[0];
-  const double V0 = S[1] * T[2] - S[2] * T[1], V1 = S[2] * T[0] - S[0] * T[2],
-               V2 = S[0] * T[1] - S[1] * T[0];
-  d0 = P[0] * U0 + P[1] * U1 + P[2] * U2;
-  d1 = (P[0] * V0 + P[1] * V1 + P[2] * V2) + (Q[0] * U0 + Q[1] * U1 + Q[2] * U2);
-  d2 = Q[0] * V0 + Q[1] * V1 + Q[2] * V2;
-}
-
-template <int N, bool ENERGY, bool STAGE, bool GEOM = false>
+template <int N, bool ENERGY, bool STAGE>
 __global__ void __launch_bounds__(Cfg<kBP1, N>::NT, HX_MINB_BP1_OF(N))
     bp1_kernel(const __grid_constant__ BP1Params<N> p) {
   using C = Cfg<kBP1, N>;
@@ -112,7 +62,6 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT, HX_MINB_BP1_OF(N))
   constexpr int QS = C::QS;
   constexpr bool QST = STAGE && QS > 0;
   extern __shared__ double smem[];
-  __shared__ double kc[GEOM ? EPB * kKC : 1];
   uint64_t* const qbar = reinterpret_cast<uint64_t*>(smem);
   double* const QT = smem + (QST ? 2 : 0);
   double* const X = QT + (QST ? EPB * n * QS : 0);
@@ -147,10 +96,7 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT, HX_MINB_BP1_OF(N))
     const int64_t e0 = int64_t(blockIdx.x) * EPB;
     const int64_t ne = min64(EPB, p.n_el - e0);
     if constexpr (!QST) prefetch_l2(p.q + e0 * n3, ne * n3 * sizeof(double));
-    if constexpr (GEOM)
-      prefetch_l2(p.verts + e0 * 24, ne * 24 * sizeof(double));
-    else
-      prefetch_l2(p.gwj + e0 * fs, ne * fs * sizeof(double));
+    prefetch_l2(p.gwj + e0 * fs, ne * fs * sizeof(double));
   }
 
   double en = 0.0;  // this thread's share of <q, A q> (ENERGY)
@@ -163,24 +109,13 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT, HX_MINB_BP1_OF(N))
         const int64_t f0 = nt * EPB;
         const int64_t nn = min64(EPB, p.n_el - f0);
         if constexpr (!QST) prefetch_l2(p.q + f0 * n3, nn * n3 * sizeof(double));
-        if constexpr (GEOM)
-          prefetch_l2(p.verts + f0 * 24, nn * 24 * sizeof(double));
-        else
-          prefetch_l2(p.gwj + f0 * fs, nn * fs * sizeof(double));
-      }
-    }
-    if constexpr (GEOM) {
-      // the tile's corner combinations; read in S3, two barriers later (the
-      // previous tile's S3 readers are past the end-of-tile barrier)
-      for (int x = tid; x < EPB * kKC; x += NT) {
-        const int el = x / kKC, r = x % kKC;
-        if (el < ne) kc[x] = corner_combo(p.verts + (e0 + el) * 24, r / 3, r % 3);
+        prefetch_l2(p.gwj + f0 * fs, nn * fs * sizeof(double));
       }
     }
     // GwJ of this thread's S3 k-line, issued early so its latency hides
     // behind S1 and S2 (one-line-per-thread shapes only).
     double w[m];
-    if constexpr (ONE_C && !GEOM) {
+    if constexpr (ONE_C) {
       const int el_c = tid / m2, ln_c = tid % m2;
       if (el_c < ne) {
         const double* g = p.gwj + (e0 + el_c) * fs + ln_c;
@@ -239,13 +174,7 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT, HX_MINB_BP1_OF(N))
       if (el >= ne) return;
       const int a = ln / m, c = ln % m;
       double wl[m];
-      if constexpr (GEOM) {
-        double d0, d1, d2;
-        line_det(kc + el * kKC, p.xg[c], p.xg[a], d0, d1, d2);
-        const double wac = p.wg[a] * p.wg[c];
-#pragma unroll
-        for (int t = 0; t < m; ++t) wl[t] = fma(p.xg[t], fma(p.xg[t], d2, d1), d0) * (wac * p.wg[t]);
-      } else if constexpr (ONE_C) {
+      if constexpr (ONE_C) {
 #pragma unroll
         for (int t = 0; t < m; ++t) wl[t] = w[t];
       } else {
@@ -308,23 +237,23 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT, HX_MINB_BP1_OF(N))
   }
 }
 
-template <int N, bool E, bool STAGE, class Prm, bool GEOM = false>
+template <int N, bool E, bool STAGE, class Prm>
 static cudaError_t launch_t(const Prm& prm, int64_t n_el, cudaStream_t s) {
   using C = Cfg<kBP1, N>;
   constexpr int smem = smem_doubles<kBP1, N>() * int(sizeof(double));
   static int blocks_per_sm = -1;
   if (blocks_per_sm < 0) {
-    cudaError_t err = cudaFuncSetAttribute(bp1_kernel<N, E, STAGE, GEOM>,
+    cudaError_t err = cudaFuncSetAttribute(bp1_kernel<N, E, STAGE>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (err != cudaSuccess) return err;
-    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &blocks_per_sm, bp1_kernel<N, E, STAGE, GEOM>, C::NT, smem);
+    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, bp1_kernel<N, E, STAGE>,
+                                                        C::NT, smem);
     if (err != cudaSuccess) return err;
     if (blocks_per_sm < 1) blocks_per_sm = 1;
   }
   const int64_t ntiles = (n_el + C::EPB - 1) / C::EPB;
   const int64_t grid = min64(ntiles, int64_t(blocks_per_sm) * sm_count());
-  bp1_kernel<N, E, STAGE, GEOM><<<unsigned(grid), C::NT, smem, s>>>(prm);
+  bp1_kernel<N, E, STAGE><<<unsigned(grid), C::NT, smem, s>>>(prm);
   return cudaGetLastError();
 }
 
@@ -340,8 +269,7 @@ static cudaError_t launch_s(const Prm& prm, int64_t n_el, cudaStream_t s) {
 
 template <int N>
 static cudaError_t launch_n(const hx_plan& P, const double* q, const double* fac, double* out,
-                            int64_t n_el, int* flag, double* energy, cudaStream_t s,
-                            const double* verts = nullptr) {
+                            int64_t n_el, int* flag, double* energy, cudaStream_t s) {
   using C = Cfg<kBP1, N>;
   constexpr int n = N + 1, m = N + 2;
   constexpr int smem = smem_doubles<kBP1, N>() * int(sizeof(double));
@@ -357,24 +285,15 @@ static cudaError_t launch_n(const hx_plan& P, const double* q, const double* fac
   prm.fac_estride = P.elem_stride;
   prm.flag = flag;
   prm.energy = energy;
-  prm.verts = verts;
-  for (int a = 0; a < m; ++a) {
-    prm.xg[a] = P.nodes[a];
-    prm.wg[a] = P.weights[a];
-  }
-  if (verts)  // on-the-fly geometry (unstaged shape)
-    return energy ? launch_t<N, true, false, BP1Params<N>, true>(prm, n_el, s)
-                  : launch_t<N, false, false, BP1Params<N>, true>(prm, n_el, s);
   return energy ? launch_s<N, true>(prm, n_el, s) : launch_s<N, false>(prm, n_el, s);
 }
 
 cudaError_t launch_bp1(const hx_plan& P, const double* q, const double* fac, double* out,
-                       int64_t n_el, int* flag, double* energy, cudaStream_t s,
-                       const double* verts) {
+                       int64_t n_el, int* flag, double* energy, cudaStream_t s) {
   switch (P.degree) {
 #define HX_CASE(N) \
   case N:          \
-    return launch_n<N>(P, q, fac, out, n_el, flag, energy, s, verts);
+    return launch_n<N>(P, q, fac, out, n_el, flag, energy, s);
     HX_CASE(1) HX_CASE(2) HX_CASE(3) HX_CASE(4) HX_CASE(5) HX_CASE(6) HX_CASE(7) HX_CASE(8)
     HX_CASE(9) HX_CASE(10) HX_CASE(11) HX_CASE(12) HX_CASE(13) HX_CASE(14) HX_CASE(15)
 #undef HX_CASE

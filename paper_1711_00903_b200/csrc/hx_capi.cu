@@ -177,18 +177,6 @@ int hx_apply(const hx_plan* P, const double* q, const double* factors, double* o
   return cuda_status(launch(*P, q, factors, out, n_el, flag, static_cast<cudaStream_t>(stream)));
 }
 
-int hx_apply_geom(const hx_plan* P, const double* q, const double* verts, double* out,
-                  int64_t n_el, int* flag, void* stream) {
-  if (!P || n_el < 0 || P->bp != HX_BP1) return HX_EINVAL;
-  if (n_el == 0) return HX_OK;
-  if (!q || !verts || !out) return HX_EINVAL;
-  if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(verts) |
-       reinterpret_cast<uintptr_t>(out)) & 7)
-    return HX_EINVAL;
-  return cuda_status(launch_bp1(*P, q, nullptr, out, n_el, flag, nullptr,
-                                static_cast<cudaStream_t>(stream), verts));
-}
-
 int hx_apply_range(const hx_plan* P, const double* q, const double* factors, double* out,
                    int64_t e_begin, int64_t e_end, int* flag, void* stream) {
   if (!P || e_begin < 0 || e_end < e_begin) return HX_EINVAL;

@@ -43,8 +43,7 @@ namespace hx {
 
 // launch the fused element kernel for elements [0, n_el) of device arrays
 cudaError_t launch_bp1(const hx_plan& P, const double* q, const double* fac, double* out,
-                       int64_t n_el, int* flag, double* energy, cudaStream_t s,
-                       const double* verts = nullptr);
+                       int64_t n_el, int* flag, double* energy, cudaStream_t s);
 cudaError_t launch_bp35(const hx_plan& P, const double* q, const double* fac, double* out,
                         int64_t n_el, int* flag, double* energy, cudaStream_t s);
 cudaError_t launch_bp3(const hx_plan& P, const double* q, const double* fac, double* out,

@@ -128,11 +128,6 @@ class OperatorInstance:
     plan: object = field(default=None, repr=False, compare=False)
     device_factors: object = field(default=None, repr=False, compare=False)
     device: object = field(default=None, repr=False, compare=False)
-    device_vertices: object = field(default=None, repr=False, compare=False)  # on-the-fly GwJ
-
-    @property
-    def geometry(self):
-        return "stored" if self.device_vertices is None else "on_the_fly"
 
     @property
     def n_q(self):
@@ -170,28 +165,14 @@ def _validate(bp, degree, variant, lam):
     check_degree(degree)
 
 
-GEOMETRIES = ("stored", "on_the_fly")
-
-
-def make_operator(bp, degree, mesh, lam=0.0, variant="fused", device=None, factors=None,
-                  geometry="stored"):
+def make_operator(bp, degree, mesh, lam=0.0, variant="fused", device=None, factors=None):
     """Assemble matrices and device-resident geometric factors.
 
     ``factors`` (optional) is a reference-layout ``(n_el, 7, m, m, m)`` array or
     ``GeometricFactors`` to upload instead of generating them on the device
     (used to feed the reference's exact factors into parity tests).
-
-    ``geometry="on_the_fly"`` (BP1.0, new -- the reference always stores
-    factors, operators.py:133): device applies recompute GwJ inside the kernel
-    from the element corners (hx_apply_geom), reading 192 bytes per element
-    instead of (N+2)^3 doubles.  Factors are still generated (validation,
-    ``op.factors``, the host-buffer path).
     """
     _validate(bp, degree, variant, lam)
-    if geometry not in GEOMETRIES:
-        raise ValueError(f"unknown geometry {geometry!r}")
-    if geometry == "on_the_fly" and (bp != BP1 or factors is not None):
-        raise ValueError("on-the-fly geometry is available for BP1.0 with mesh-derived factors")
     import torch
 
     dev = torch.device("cuda", torch.cuda.current_device()) if device is None \
@@ -244,8 +225,7 @@ def make_operator(bp, degree, mesh, lam=0.0, variant="fused", device=None, facto
 
     geo = GeometricFactors(rule.kind, q, rule.weights, loader=host_view)
     return OperatorInstance(bp, degree, float(lam), interp, diff, geo, variant, n_el,
-                            plan=plan, device_factors=packed, device=dev,
-                            device_vertices=verts if geometry == "on_the_fly" else None)
+                            plan=plan, device_factors=packed, device=dev)
 
 
 def _charge(op, counters):
@@ -262,11 +242,6 @@ def apply_device(op, q, out, flag=None, stream=None):
     This is what the harness times."""
     if stream is None:
         stream = _stream(op.device)
-    if op.device_vertices is not None:
-        _native.check(_native.lib().hx_apply_geom(
-            op.plan.handle, _native.ptr(q), _native.ptr(op.device_vertices), _native.ptr(out),
-            op.n_el, _native.ptr(flag), stream), "hx_apply_geom")
-        return
     _native.check(_native.lib().hx_apply(
         op.plan.handle, _native.ptr(q), _native.ptr(op.device_factors), _native.ptr(out),
         op.n_el, _native.ptr(flag), stream), "hx_apply")

@@ -119,8 +119,3 @@ def test_element_helper_validation_before_device():
         hx.project_to_gll(np.zeros((4, 4, 4)), mat)
     with pytest.raises(ValueError):
         hx.interpolate_to_gl(np.zeros((4, 4, 4)), np.zeros((4, 4)))
-
-
-def test_geometry_option_validation(perturbed_single):
-    with pytest.raises(ValueError):
-        hx.make_operator(hx.BP1, 2, perturbed_single, geometry="analytic")

@@ -329,41 +329,3 @@ def test_host_path_concurrent_threads_on_one_plan(mesh3):
     assert not errors, errors
     for got, ref in zip(outs, want):
         np.testing.assert_array_equal(got, ref)
-
-
-@pytest.mark.parametrize("deg", range(1, 16))
-def test_on_the_fly_geometry_bp1_matches_oracle(deg, mesh3):
-    """BP1.0 with GwJ recomputed in-kernel from the corners (hx_apply_geom)
-    == the oracle on the reference factors, every degree, ragged counts."""
-    rng = np.random.default_rng(200 + deg)
-    for n_el in (1, 13, 27):
-        m = sub_mesh(mesh3, n_el)
-        op = hx.make_operator(hx.BP1, deg, m, lam=0.0, geometry="on_the_fly")
-        assert op.geometry == "on_the_fly"
-        q = rng.standard_normal((n_el, op.n_p))
-        got = dev_apply(op, q)
-        ref = oracle_apply(op, q)
-        assert orc.rel_l2(got, ref) <= PARITY, (deg, n_el, orc.rel_l2(got, ref))
-        stored = dev_apply(hx.make_operator(hx.BP1, deg, m, lam=0.0), q)
-        assert orc.rel_l2(got, stored) <= 1e-13
-
-
-def test_on_the_fly_geometry_full_size_and_errors():
-    mesh = hx.perturb_mesh(hx.build_cube_mesh(32, 2.0), amplitude=0.15, seed=7)
-    op = hx.make_operator(hx.BP1, 7, mesh, geometry="on_the_fly")
-    ref_op = hx.make_operator(hx.BP1, 7, mesh)
-    q = hx.FieldVector.random(mesh.n_el, op.n_p, seed=0).to_device()
-    a = hx.apply_operator(op, q).data
-    b = hx.apply_operator(ref_op, q).data
-    assert float(torch.linalg.norm(a - b) / torch.linalg.norm(b)) <= 1e-13
-    bad = q.data.clone()
-    bad[3, 7] = float("nan")
-    with pytest.raises(ValueError):
-        hx.apply_operator(op, hx.FieldVector(mesh.n_el, op.n_p, bad))
-    with pytest.raises(ValueError):
-        hx.make_operator(hx.BP35, 3, sub_mesh(mesh, 2), geometry="on_the_fly")
-    op35 = hx.make_operator(hx.BP35, 3, sub_mesh(mesh, 2))
-    x = torch.zeros((2, 64), dtype=torch.float64, device="cuda")
-    v = torch.zeros((2, 8, 3), dtype=torch.float64, device="cuda")
-    assert _native.lib().hx_apply_geom(op35.plan.handle, _native.ptr(x), _native.ptr(v),
-                                       _native.ptr(x), 2, None, None) == _native.HX_EINVAL
