@@ -99,7 +99,9 @@ int hx_apply_range(const hx_plan* plan, const double* q, const double* factors, 
 /* End-to-end variant on HOST q / out (page-locked for full overlap): chunks of
  * up to `chunk_el` elements (ramped up and down at the ends) are copied in,
  * applied and copied back on a three-stream pipeline with three buffer slots,
- * so PCIe transfers in both directions overlap each other and the kernel.  `work` is a device buffer of
+ * so PCIe transfers in both directions overlap each other and the kernel.
+ * Back-to-back calls with the same `work` and `chunk_el` continue the slot
+ * sequence: the next call's H2D copies start while the previous call drains.  `work` is a device buffer of
  * at least hx_apply_host_workspace(plan, chunk_el) bytes; `stream` is made to
  * wait for the whole pipeline.                                              */
 int64_t hx_apply_host_workspace(const hx_plan* plan, int64_t chunk_el);

@@ -285,21 +285,30 @@ int hx_apply_host(const hx_plan* Pc, const double* q_host, const double* factors
   if ((err = cudaEventCreateWithFlags(&start, cudaEventDisableTiming)) != cudaSuccess)
     return cuda_status(err);
   cudaEventRecord(start, caller);
-  cudaStreamWaitEvent(s_in, start, 0);
+  // H2D copies read host memory into our slots: they need only the slot
+  // events -- unless the workspace layout changed since the last call, then
+  // they start after the caller's queue like the kernels and D2H copies
+  const bool cont = P->pipe_work == work && P->pipe_chunk == chunk_el;
+  if (!cont) {
+    cudaStreamWaitEvent(s_in, start, 0);
+    P->pipe_seq = 0;
+  }
   cudaStreamWaitEvent(s_k, start, 0);
   cudaStreamWaitEvent(s_out, start, 0);
   const std::vector<int64_t> sched = chunk_schedule(n_el, chunk_el);
   const int64_t nchunks = int64_t(sched.size());
   int64_t e0 = 0;
+  const int64_t seq0 = P->pipe_seq;
   for (int64_t c = 0; c < nchunks; ++c) {
-    const int slot = int(c % S);
+    const int64_t g = seq0 + c;  // slot sequence number across calls
+    const int slot = int(g % S);
     const int64_t ne = sched[c];
     const size_t bytes = size_t(ne * n3) * sizeof(double);
-    if (c >= S) cudaStreamWaitEvent(s_in, e_k[slot], 0);  // kernel c-S done reading wq[slot]
+    if (g >= S) cudaStreamWaitEvent(s_in, e_k[slot], 0);  // kernel g-S done reading wq[slot]
     cudaMemcpyAsync(wq[slot], q_host + e0 * n3, bytes, cudaMemcpyHostToDevice, s_in);
     cudaEventRecord(e_in[slot], s_in);
     cudaStreamWaitEvent(s_k, e_in[slot], 0);
-    if (c >= S) cudaStreamWaitEvent(s_k, e_out[slot], 0);  // D2H c-S done with wo[slot]
+    if (g >= S) cudaStreamWaitEvent(s_k, e_out[slot], 0);  // D2H g-S done with wo[slot]
     if ((err = launch(*P, wq[slot], factors + e0 * P->elem_stride, wo[slot], ne, flag, s_k)) !=
         cudaSuccess) {
       cudaEventDestroy(start);
@@ -312,7 +321,10 @@ int hx_apply_host(const hx_plan* Pc, const double* q_host, const double* factors
     e0 += ne;
   }
   // D2H is in order on one stream: its last chunk done means all are
-  cudaStreamWaitEvent(caller, e_out[(nchunks - 1) % S], 0);
+  cudaStreamWaitEvent(caller, e_out[(seq0 + nchunks - 1) % S], 0);
+  P->pipe_seq = seq0 + nchunks;
+  P->pipe_work = work;
+  P->pipe_chunk = chunk_el;
   cudaEventDestroy(start);
   return cuda_status(cudaGetLastError());
 }

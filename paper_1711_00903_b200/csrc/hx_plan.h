@@ -37,6 +37,13 @@ struct hx_plan {
   cudaEvent_t ev[3][hx_host_slots];
   bool pipe_ready;
   std::mutex pipe_mu;
+  // chunk slots persist across hx_apply_host calls: a call that reuses the
+  // previous call's workspace and chunk size continues the slot sequence, so
+  // its H2D copies only wait for the slots they reuse (not for the whole
+  // previous call) and back-to-back calls overlap their transfers
+  int64_t pipe_seq = 0;
+  const void* pipe_work = nullptr;
+  int64_t pipe_chunk = 0;
 };
 
 namespace hx {
