@@ -91,7 +91,11 @@ def main(run_dir, dest, launches=None):
                 rb = to_bytes(*rec["dram__bytes_read.sum"])
                 wb = to_bytes(*rec["dram__bytes_write.sum"])
                 short = name.split("(")[0].replace("void ", "").replace("hx::", "")
-                traffic[short] = rb + wb
+                # canonical key: kernel<N> (the other template flags -- energy,
+                # staging -- do not change the plain apply's traffic)
+                base, _, targs = short.partition("<")
+                key = f"{base}<{targs.split(',')[0].rstrip('>').strip()}>" if targs else short
+                traffic[key] = rb + wb
     if launches and os.path.exists(launches):
         lines.append("## Launch list (`gpu__time_duration.sum`, cold-cache, serialised)")
         lines.append("")
