@@ -15,6 +15,12 @@
 // projection are fused in registers in S3, so the GL-point tensor never
 // leaves the thread that owns its k-line.  The contraction order differs from
 // the reference's (j, i, k) only by floating-point reassociation.
+//
+// Cfg::ORD picks the lane order of the shared-memory-only i-line stages S2/S4
+// jointly with the strides (tools/gen_layouts.py): at N=7 the k-paired order
+// with k-paired X/Y layouts makes every stage bank-conflict free (r10:
+// 173.6 -> 185.3 GDOF/s).  Cfg::QS > 0 would stage q through shared memory
+// with the bulk-copy engine (measured slower, off: profiles/tuning).
 #include "hx_common.cuh"
 #include "hx_plan.h"
 
