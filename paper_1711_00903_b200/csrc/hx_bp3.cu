@@ -38,16 +38,6 @@
 #ifndef HX_PF_BP3
 #define HX_PF_BP3 2  // stage at which a tile's factors are prefetched into L2
 #endif
-// HX_BP3_FSL > 0: the first FSL factor slots of a tile are staged in shared
-// memory by the bulk-copy engine one tile ahead (issued when S5 of the
-// previous tile has consumed them), so S5 reads them without long-scoreboard
-// waits; the other slots are still read from L2.  Degree HX_BP3_FSL_N only.
-#ifndef HX_BP3_FSL
-#define HX_BP3_FSL 0
-#endif
-#ifndef HX_BP3_FSL_N
-#define HX_BP3_FSL_N 7
-#endif
 // HX_MINB_BP3 overrides Cfg<>::MINB (resident CTAs per SM for the register
 // budget) in tuning builds only.
 #ifdef HX_MINB_BP3
@@ -75,20 +65,6 @@ struct BP3Params {
   double* energy;  // per-CTA partials of <q, A q> (ENERGY instantiation only)
 };
 
-template <int N>
-constexpr int bp3_fsl() {
-  return N == HX_BP3_FSL_N ? HX_BP3_FSL : 0;
-}
-template <int N>
-constexpr int bp3_slot_doubles() {
-  return ((N + 2) * (N + 2) * (N + 2) + 1) & ~1;  // hx_plan::slot_stride
-}
-template <int N>
-constexpr int bp3_smem_doubles() {
-  constexpr int F = bp3_fsl<N>();
-  return smem_doubles<kBP3, N>() + (F > 0 ? 2 + Cfg<kBP3, N>::EPB * F * bp3_slot_doubles<N>() : 0);
-}
-
 template <int N, bool ENERGY>
 __global__ void __launch_bounds__(Cfg<kBP3, N>::NT, HX_MINB_BP3_OF(N))
     bp3_kernel(const __grid_constant__ BP3Params<N> p) {
@@ -98,36 +74,14 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT, HX_MINB_BP3_OF(N))
   constexpr Lay LX = C::L[0], LQR = C::L[1], LY = C::L[2], LQS = C::L[3], LT = C::L[4],
                 LZ = C::L[5];
   constexpr int EA = C::EBUF[0], EB = C::EBUF[1], EC = C::EBUF[2];
-  constexpr int FSL = bp3_fsl<N>(), SSD = bp3_slot_doubles<N>();
   extern __shared__ double smem[];
-  uint64_t* const fbar = reinterpret_cast<uint64_t*>(smem);
-  double* const F = smem + (FSL > 0 ? 2 : 0);  // [EPB][FSL][SSD]
-  double* const A = F + (FSL > 0 ? EPB * FSL * SSD : 0);
+  double* const A = smem;
   double* const B = A + EPB * EA;
   double* const Cs = B + EPB * EB;
 
   const int tid = threadIdx.x;
   const int64_t ntiles = (p.n_el + EPB - 1) / EPB;
   const int64_t fs = p.fac_estride, ss = p.fac_sstride;
-
-  // FSL > 0: thread 0 stages tile t's leading factor slots (contiguous per
-  // element: slot_stride == SSD, checked by the launcher)
-  auto stage_f = [&](int64_t t) {
-    if constexpr (FSL > 0) {
-      const int64_t f0 = t * EPB;
-      const int nn = int(min64(EPB, p.n_el - f0));
-      constexpr unsigned bytes = FSL * SSD * sizeof(double);
-      mbar_arrive_expect_tx(fbar, nn * bytes);
-      const uint64_t pol = l2_evict_first_policy();
-      for (int e = 0; e < nn; ++e) bulk_g2s(F + e * FSL * SSD, p.fac + (f0 + e) * fs, bytes, fbar, pol);
-    }
-  };
-  if constexpr (FSL > 0) {
-    if (tid == 0) mbar_init(fbar, 1);
-    __syncthreads();
-    if (tid == 0 && blockIdx.x < ntiles) stage_f(blockIdx.x);
-  }
-  unsigned fphase = 0;
 
   // L2 prefetch schedule (see hx_bp35.cu): a tile's factors are requested
   // when S2 starts (consumed in S5), the next tile's q when S6 starts.
@@ -136,16 +90,6 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT, HX_MINB_BP3_OF(N))
     const int64_t ne = min64(EPB, p.n_el - e0);
     prefetch_l2(p.q + e0 * n3, ne * n3 * sizeof(double));
   }
-
-  // L2 prefetch of a tile's unstaged factor slots
-  auto prefetch_fac = [&](int64_t e0, int64_t ne) {
-    if constexpr (FSL == 0) {
-      prefetch_l2(p.fac + e0 * fs, ne * fs * sizeof(double));
-    } else if constexpr (FSL < 7) {
-      for (int64_t e = 0; e < ne; ++e)
-        prefetch_l2(p.fac + (e0 + e) * fs + FSL * ss, (7 - FSL) * ss * sizeof(double));
-    }
-  };
 
   const int el_a = tid / n2, ln_a = tid % n2;
   const int el_b = tid / (n * m), ln_b = tid % (n * m);
@@ -164,7 +108,7 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT, HX_MINB_BP3_OF(N))
     double* const Cc = Cs + el_c * EC;
 
     // ---- S1: j-lines (k, i): interpolate along s
-    if (HX_PF_BP3 == 1 && tid == 0) prefetch_fac(e0, ne);
+    if (HX_PF_BP3 == 1 && tid == 0) prefetch_l2(p.fac + e0 * fs, ne * fs * sizeof(double));
     if (el_a < ne) {
       const int k = ln_a / n, i = ln_a % n;
       const double* src = p.q + (e0 + el_a) * n3 + k * n2 + i;
@@ -180,7 +124,7 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT, HX_MINB_BP3_OF(N))
     }
     __syncthreads();
     // ---- S2: i-lines (k, a): interpolate along r
-    if (HX_PF_BP3 == 2 && tid == 0) prefetch_fac(e0, ne);
+    if (HX_PF_BP3 == 2 && tid == 0) prefetch_l2(p.fac + e0 * fs, ne * fs * sizeof(double));
     if (el_b < ne) {
       int k, a;
       iline_coords<n, m, C::ORD>(ln_b, k, a);
@@ -195,7 +139,7 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT, HX_MINB_BP3_OF(N))
     }
     __syncthreads();
     // ---- S3: k-lines (a, c): interpolate along t
-    if (HX_PF_BP3 == 3 && tid == 0) prefetch_fac(e0, ne);
+    if (HX_PF_BP3 == 3 && tid == 0) prefetch_l2(p.fac + e0 * fs, ne * fs * sizeof(double));
     double acc[m];
     constexpr bool kReread = N >= HX_BP3_REREAD_MIN_N;
     double tvc[kReread ? 1 : m], ttc[kReread ? 1 : m];  // carried S3 -> S5 unless kReread
@@ -218,7 +162,7 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT, HX_MINB_BP3_OF(N))
     }
     __syncthreads();
     // ---- S4: r- and s-derivatives of T
-    if (HX_PF_BP3 == 4 && tid == 0) prefetch_fac(e0, ne);
+    if (HX_PF_BP3 == 4 && tid == 0) prefetch_l2(p.fac + e0 * fs, ne * fs * sizeof(double));
     if (act_c) {
       const int kk = ln_c / m, r = ln_c % m;
       double x[m], y[m];
@@ -243,8 +187,6 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT, HX_MINB_BP3_OF(N))
       double* qrl = Ac + ca * LQR.s1 + cc;
       double* qsl = Bc + ca * LQS.s1 + cc;
       const double* g = p.fac + (e0 + el_c) * fs + ln_c;
-      const double* gs = F + el_c * FSL * SSD + ln_c;  // staged slots
-      if constexpr (FSL > 0) mbar_wait(fbar, fphase);
       double rqt[m], tv[m], tt[m];
       if constexpr (kReread) {
         // re-read this thread's own T k-line (still intact in C)
@@ -262,11 +204,9 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT, HX_MINB_BP3_OF(N))
 #pragma unroll
       for (int t = 0; t < m; ++t) {
         const double* gk = g + t * m2;
-        const double* gq = gs + t * m2;
-        auto fac = [&](int slot) { return slot < FSL ? gq[slot * SSD] : gk[slot * ss]; };
-        const double grr = fac(0), grs = fac(1), grt = fac(2);
-        const double gss = fac(3), gst = fac(4), gtt = fac(5);
-        const double gwj = fac(6);
+        const double grr = gk[0], grs = gk[ss], grt = gk[2 * ss];
+        const double gss = gk[3 * ss], gst = gk[4 * ss], gtt = gk[5 * ss];
+        const double gwj = gk[6 * ss];
         const double qr = qrl[LQR.kofs(t)], qs = qsl[LQS.kofs(t)], qt = tt[t];
         const double rqr = grr * qr + grs * qs + grt * qt;
         const double rqs = grs * qr + gss * qs + gst * qt;
@@ -283,14 +223,6 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT, HX_MINB_BP3_OF(N))
       for (int t = 0; t < m; ++t) acc[t] += tv[t];
     }
     __syncthreads();
-    if constexpr (FSL > 0) {
-      // the staged slots have been consumed: fetch the next tile's
-      fphase ^= 1u;
-      if (tid == 0 && tile + gridDim.x < ntiles) {
-        fence_proxy_async_smem();
-        stage_f(tile + gridDim.x);
-      }
-    }
     // ---- S6: transposed r- and s-derivatives in place
     if (tid == 0) {
       const int64_t nt = tile + gridDim.x;
@@ -366,7 +298,7 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT, HX_MINB_BP3_OF(N))
 template <int N, bool E, class Prm>
 static cudaError_t launch_t(const Prm& prm, int64_t n_el, cudaStream_t s) {
   using C = Cfg<kBP3, N>;
-  constexpr int smem = bp3_smem_doubles<N>() * int(sizeof(double));
+  constexpr int smem = smem_doubles<kBP3, N>() * int(sizeof(double));
   static int blocks_per_sm = -1;
   if (blocks_per_sm < 0) {
     cudaError_t err = cudaFuncSetAttribute(bp3_kernel<N, E>,
@@ -388,7 +320,7 @@ static cudaError_t launch_n(const hx_plan& P, const double* q, const double* fac
                             int64_t n_el, int* flag, double* energy, cudaStream_t s) {
   using C = Cfg<kBP3, N>;
   constexpr int n = N + 1, m = N + 2;
-  constexpr int smem = bp3_smem_doubles<N>() * int(sizeof(double));
+  constexpr int smem = smem_doubles<kBP3, N>() * int(sizeof(double));
   BP3Params<N> prm;
   double it[n * m], dt[m * m];
   fill_fold(prm.I, P.interp);
@@ -403,7 +335,6 @@ static cudaError_t launch_n(const hx_plan& P, const double* q, const double* fac
   prm.n_el = n_el;
   prm.fac_estride = P.elem_stride;
   prm.fac_sstride = P.slot_stride;
-  if (bp3_fsl<N>() > 0 && P.slot_stride != bp3_slot_doubles<N>()) return cudaErrorInvalidValue;
   prm.lam = P.lam;
   prm.flag = flag;
   prm.energy = energy;
