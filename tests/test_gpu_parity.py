@@ -329,3 +329,38 @@ def test_host_path_concurrent_threads_on_one_plan(mesh3):
     assert not errors, errors
     for got, ref in zip(outs, want):
         np.testing.assert_array_equal(got, ref)
+
+
+@pytest.mark.parametrize("bp,deg,n_el", [
+    # q / out offsets e*n^3 and factor offsets e*elem_stride pass 2^31
+    (hx.BP1, 15, 7 * 75_715),
+    # factor offsets e*elem_stride pass 2^31 (elem_stride 3584 / 5110)
+    (hx.BP35, 7, 7 * 87_000),
+    (hx.BP3, 7, 7 * 61_000),
+])
+def test_64bit_offsets_periodic_mesh(bp, deg, n_el, mesh3):
+    """Maximum-size edge case: element counts whose double offsets exceed
+    2^31 (17-56 GB on the device).  The mesh and q repeat with period 7, so
+    A q must repeat bitwise (element-locality, reference operators.py:300-302)
+    and its first period must match the oracle; a non-finite value in the
+    last element is still detected (operators.py:317-318)."""
+    period = 7
+    small = sub_mesh(mesh3, period)
+    reps = n_el // period
+    mesh = hx.HexMesh(n_el, np.tile(small.vertices, (reps, 1, 1)), small.extent)
+    op = hx.make_operator(bp, deg, mesh, lam=0.7)
+    assert max(n_el * op.n_p, n_el * op.plan.elem_stride) > 2 ** 31
+    q7 = np.random.default_rng(deg).standard_normal((period, op.n_p))
+    q = torch.from_numpy(q7).cuda().repeat(reps, 1)
+    out = torch.empty_like(q)
+    hx.apply_device(op, q, out)
+    torch.cuda.synchronize()
+    assert torch.equal(out.view(reps, period, -1), out[:period].expand(reps, period, -1))
+    ref = oracle_apply(hx.make_operator(bp, deg, small, lam=0.7), q7)
+    assert orc.rel_l2(out[:period].cpu().numpy(), ref) <= PARITY
+    del out
+    q[-1, -1] = float("inf")
+    with pytest.raises(ValueError):
+        hx.apply_operator(op, hx.FieldVector(n_el, op.n_p, q))
+    del q, op
+    torch.cuda.empty_cache()
