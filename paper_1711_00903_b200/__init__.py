@@ -6,7 +6,8 @@ backed by hand-written sm_100a kernels behind the C ABI in
 ``include/hexbench_b200.h``.
 """
 
-from .basis import MAX_DEGREE, OperatorMatrix, diff_matrix_gl, diff_matrix_gll, interp_matrix
+from .basis import (MAX_DEGREE, OperatorMatrix, contract_dim, diff_matrix_gl, diff_matrix_gll,
+                    interp_matrix)
 from .mesh import (FACTOR_NAMES, DegenerateGeometryError, GeometricFactors, HexMesh,
                    build_cube_mesh, geometric_factors, perturb_mesh, trilinear_jacobian,
                    trilinear_map)
@@ -14,7 +15,8 @@ from .operators import (AccessCounters, FieldVector, OperatorInstance, Unsupport
                         apply_baseline, apply_bp1, apply_bp3, apply_bp35, apply_device, apply_host,
                         apply_operator, interpolate_to_gl, make_operator,
                         project_to_gll)
-from .perf import (BENCHMARKS, BP1, BP3, BP35, VARIANTS, RooflinePoint, RooflineSeries,
+from .perf import (BENCHMARKS, BP1, BP3, BP35, VARIANTS, BandwidthCalibration, RooflinePoint,
+                   RooflineSeries, measure_stream_bandwidth,
                    TrafficModel, element_counters, flop_model, roofline_global,
                    roofline_series, roofline_shared, scratch_traffic, shared_bandwidth_ansatz,
                    traffic)

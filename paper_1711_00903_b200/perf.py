@@ -79,6 +79,63 @@ def flop_model(bp, variant, degree):
     return 2 * interp + 12 * m ** 4 + 20 * m ** 3
 
 
+# nominal B200 HBM3e bandwidth (the calibration's `theoretical_peak`)
+B200_PEAK_BANDWIDTH = 8.0e12
+
+
+@dataclass(frozen=True)
+class BandwidthCalibration:
+    """Result of :func:`measure_stream_bandwidth` (reference perf.py:46-51)."""
+
+    bytes_transferred: int
+    trial_times: list
+    mean_bandwidth: float
+    theoretical_peak: float = DEFAULT_PEAK_BANDWIDTH
+
+
+def measure_stream_bandwidth(nbytes, trials=10, device=None):
+    """Streaming-bandwidth calibration (reference perf.py:120-143).
+
+    Same contract as the reference -- at least 1 MiB and 3 trials
+    (``ValueError``), ``MemoryError`` when the buffers cannot be allocated,
+    one untimed warm-up pass, ``mean_bandwidth`` = mean of the per-trial
+    ``bytes_transferred / time`` -- but the copy is a device-to-device copy
+    of ``nbytes`` on the GPU the operators run on (the reference copies host
+    memory), timed with CUDA events behind a GPU spacer so host launch
+    latency is not timed.  ``bytes_transferred`` counts the bytes copied (one
+    way), as the reference does; the copy moves twice that through HBM, the
+    convention ``TrafficModel.copy_equivalent_bytes`` accounts for.
+    """
+    if nbytes < 1 << 20:
+        raise ValueError("use at least 1 MiB for a meaningful measurement")
+    if trials < 3:
+        raise ValueError("need at least 3 trials")
+    import torch
+    count = nbytes // 8
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None \
+        else torch.device(device)
+    try:
+        src = torch.randn(count, dtype=torch.float64, device=dev)
+        dst = torch.empty_like(src)
+    except torch.OutOfMemoryError as exc:
+        raise MemoryError("could not allocate calibration buffers") from exc
+    with torch.cuda.device(dev):
+        dst.copy_(src)  # warm-up
+        times = []
+        for _ in range(trials):
+            start = torch.cuda.Event(enable_timing=True)
+            stop = torch.cuda.Event(enable_timing=True)
+            torch.cuda._sleep(200_000)  # spacer: the copy is queued before `start`
+            start.record()
+            dst.copy_(src)
+            stop.record()
+            stop.synchronize()
+            times.append(start.elapsed_time(stop) * 1e-3)
+    rates = [8 * count / t for t in times]
+    return BandwidthCalibration(8 * count, times, float(sum(rates) / len(rates)),
+                                B200_PEAK_BANDWIDTH)
+
+
 def roofline_global(b_gl, flops, d_r, d_w):
     if b_gl <= 0 or flops <= 0:
         raise ValueError("bandwidth and FLOPs must be positive")

@@ -16,7 +16,11 @@ def test_public_names_mirror_reference():
                  "DegenerateGeometryError", "HexMesh", "GeometricFactors", "gl_rule",
                  "gll_rule", "lagrange_eval", "lagrange_deriv", "interp_matrix",
                  "diff_matrix_gll", "diff_matrix_gl", "traffic", "flop_model",
-                 "roofline_global", "roofline_shared", "shared_bandwidth_ansatz"):
+                 "roofline_global", "roofline_shared", "shared_bandwidth_ansatz",
+                 "contract_dim", "measure_stream_bandwidth", "BandwidthCalibration",
+                 "roofline_series", "RooflineSeries", "TrafficModel", "QuadratureRule",
+                 "legendre_and_derivative", "OperatorMatrix", "interpolate_to_gl",
+                 "project_to_gll"):
         assert hasattr(hx, name), name
     assert hx.BENCHMARKS == ("BP1.0", "BP3.5", "BP3.0")
     assert hx.VARIANTS == ("baseline", "fused", "symfused")
@@ -119,3 +123,71 @@ def test_element_helper_validation_before_device():
         hx.project_to_gll(np.zeros((4, 4, 4)), mat)
     with pytest.raises(ValueError):
         hx.interpolate_to_gl(np.zeros((4, 4, 4)), np.zeros((4, 4)))
+
+
+def _brute_contract(mat, t, axis):
+    """Triple loop (reference test_reference_ops.py brute_force_contract)."""
+    shape = list(t.shape)
+    shape[axis] = mat.shape[0]
+    out = np.zeros(shape)
+    for idx in np.ndindex(*shape):
+        src = list(idx)
+        acc = 0.0
+        for b in range(t.shape[axis]):
+            src[axis] = b
+            acc += mat[idx[axis], b] * t[tuple(src)]
+        out[idx] = acc
+    return out
+
+
+@pytest.mark.parametrize("axis", [0, 1, 2])
+def test_contract_dim_known_answers(axis):
+    """reference test_reference_ops.py:80-122: identity, constants through I,
+    triple loop, adjointness, Kronecker form; torch tensors give the same."""
+    import torch
+    rng = np.random.default_rng(axis)
+    t = rng.standard_normal((3, 3, 3))
+    np.testing.assert_array_equal(hx.contract_dim(np.eye(3), t, axis), t)
+    np.testing.assert_allclose(hx.contract_dim(hx.interp_matrix(2), np.full((3, 3, 3), 4.2), axis),
+                               4.2, atol=1e-13)
+    t2 = rng.standard_normal((2, 2, 2))
+    mat = rng.standard_normal((3, 2))
+    got = hx.contract_dim(mat, t2, axis)
+    np.testing.assert_allclose(got, _brute_contract(mat, t2, axis), atol=1e-14)
+    np.testing.assert_allclose(hx.contract_dim(mat, torch.from_numpy(t2), axis).numpy(), got,
+                               atol=1e-15)
+    m = rng.standard_normal((5, 4))
+    u = rng.standard_normal((4, 4, 4))
+    shape = [4, 4, 4]
+    shape[axis] = 5
+    v = rng.standard_normal(shape)
+    lhs = np.vdot(hx.contract_dim(m, u, axis), v)
+    rhs = np.vdot(u, hx.contract_dim(m.T, v, axis))
+    assert abs(lhs - rhs) < 1e-12 * max(1.0, abs(lhs))
+
+
+@pytest.mark.parametrize("degree", [1, 2, 3, 4])
+def test_contract_dim_triple_is_kronecker(degree):
+    m = hx.interp_matrix(degree).entries
+    n = degree + 1
+    u = np.random.default_rng(degree).standard_normal((n, n, n))
+    t = hx.contract_dim(m, hx.contract_dim(m, hx.contract_dim(m, u, 1), 2), 0)
+    np.testing.assert_allclose(t.ravel(), np.kron(m, np.kron(m, m)) @ u.ravel(), atol=1e-12)
+
+
+def test_contract_dim_errors():
+    rng = np.random.default_rng(0)
+    with pytest.raises(ValueError):
+        hx.contract_dim(np.ones((3, 4)), rng.standard_normal((3, 3, 3)), 0)
+    with pytest.raises(ValueError):
+        hx.contract_dim(np.ones((3, 3)), rng.standard_normal((3, 3)), 0)
+    with pytest.raises(ValueError):
+        hx.contract_dim(np.ones((3, 3)), rng.standard_normal((3, 3, 3)), 3)
+
+
+def test_measure_stream_bandwidth_validation():
+    """reference test_perf.py:163-167 (checked before any allocation)."""
+    with pytest.raises(ValueError):
+        hx.measure_stream_bandwidth(1024)
+    with pytest.raises(ValueError):
+        hx.measure_stream_bandwidth(1 << 22, trials=2)

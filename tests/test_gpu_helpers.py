@@ -111,3 +111,28 @@ def test_errors():
         hx.interpolate_to_gl(np.full((4, 4, 4), np.nan), mat)  # non-finite
     with pytest.raises(ValueError):
         hx.interpolate_to_gl(np.zeros((4, 4, 4)), np.ones((5, 4)) + np.eye(5, 4))  # not centro
+
+
+def test_measure_stream_bandwidth():
+    """reference test_perf.py:149-161 on the device copy calibration."""
+    cal = hx.measure_stream_bandwidth(1 << 22, trials=5)
+    assert cal.mean_bandwidth > 0 and np.isfinite(cal.mean_bandwidth)
+    assert len(cal.trial_times) == 5 and all(t > 0 for t in cal.trial_times)
+    rates = [cal.bytes_transferred / t for t in cal.trial_times]
+    assert min(rates) <= cal.mean_bandwidth <= max(rates)
+    a = hx.measure_stream_bandwidth(1 << 22, trials=5).mean_bandwidth
+    b = hx.measure_stream_bandwidth(1 << 23, trials=5).mean_bandwidth
+    assert 0.3 < b / a < 3.0
+    big = hx.measure_stream_bandwidth(1 << 30, trials=5)
+    # one-way bytes / time: half the HBM traffic of the copy, below the peak
+    assert 1e12 < big.mean_bandwidth < big.theoretical_peak
+
+
+def test_contract_dim_on_device():
+    mat = hx.interp_matrix(7)
+    u = np.random.default_rng(0).standard_normal((8, 8, 8))
+    for axis in range(3):
+        got = hx.contract_dim(mat, torch.from_numpy(u).cuda(), axis)
+        assert got.is_cuda
+        np.testing.assert_allclose(got.cpu().numpy(), hx.contract_dim(mat, u, axis),
+                                   rtol=0, atol=1e-13)
