@@ -4,6 +4,7 @@ schema of the reference's ``hexbench bench`` / ``hexbench roofline``
 
     python -m paper_1711_00903_b200.report bench --bp 3.5 --degrees 7 --elements 32
     python -m paper_1711_00903_b200.report roofline --bp 1.0 --degrees 1..15 --elements 16
+    python -m paper_1711_00903_b200.report calibrate --bytes 1073741824
 
 Differences from the reference, all additive: ``wall_time_*`` are CUDA-event
 times of device-resident applies, ``bandwidth_bytes_per_s`` is the measured
@@ -151,7 +152,24 @@ def main(argv=None):
         p.add_argument("--bandwidth", type=float, default=None, help="GB/s (else measured)")
         p.add_argument("--out", default=None)
         p.add_argument("--format", choices=["json", "csv"], default="json")
+    p = sub.add_parser("calibrate")  # cli.py:85-88, 350-366
+    p.add_argument("--bytes", type=int, default=1 << 27)
+    p.add_argument("--repeats", type=int, default=10)
+    p.add_argument("--out", default=None)
+    p.add_argument("--format", choices=["json", "csv"], default="json")
     args = ap.parse_args(argv)
+    if args.command == "calibrate":
+        try:
+            cal = perf.measure_stream_bandwidth(args.bytes, trials=args.repeats)
+        except (MemoryError, ValueError) as exc:
+            print(f"error: {exc}", file=sys.stderr)
+            return 3 if isinstance(exc, MemoryError) else 2  # EXIT_RESOURCE / EXIT_USAGE
+        payload = {"command": "calibrate", "bytes": cal.bytes_transferred,
+                   "trial_times_s": cal.trial_times, "mean_bytes_per_s": cal.mean_bandwidth,
+                   "theoretical_peak_bytes_per_s": cal.theoretical_peak, "machine": _machine()}
+        header = ("trial", "time_s", "bytes_per_s")
+        rows = [(i, t, cal.bytes_transferred / t) for i, t in enumerate(cal.trial_times)]
+        return _emit(payload, header, rows, args)
     bps = list(perf.BENCHMARKS) if args.bp == "all" else [_BP_FLAG[args.bp]]
     bw = None if args.bandwidth is None else args.bandwidth * 1e9
     if args.command == "bench":
@@ -178,6 +196,10 @@ def main(argv=None):
         header = ("bp", "N", "F", "bytes", "R_global", "R_shared")
         rows = [(s.bp, p.degree, p.flops, p.bytes_moved, p.r_global, p.r_shared)
                 for s in series for p in s.points]
+    return _emit(payload, header, rows, args)
+
+
+def _emit(payload, header, rows, args):
     if args.format == "csv":
         fh = sys.stdout if args.out is None else open(args.out, "w", newline="")
         w = csv.writer(fh)

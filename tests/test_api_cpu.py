@@ -191,3 +191,10 @@ def test_measure_stream_bandwidth_validation():
         hx.measure_stream_bandwidth(1024)
     with pytest.raises(ValueError):
         hx.measure_stream_bandwidth(1 << 22, trials=2)
+
+
+def test_report_calibrate_usage_errors():
+    """The calibrate command's usage exits (reference cli.py:350-355) need no GPU."""
+    from paper_1711_00903_b200.report import main
+    assert main(["calibrate", "--bytes", "100"]) == 2
+    assert main(["calibrate", "--bytes", str(1 << 22), "--repeats", "2"]) == 2

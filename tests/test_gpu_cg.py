@@ -132,6 +132,12 @@ def test_report_cli_json_and_csv(tmp_path):
     assert rows[0] == ["bp", "N", "F", "bytes", "R_global", "R_shared"]
     assert [int(r[1]) for r in rows[1:]] == [1, 2, 3]
     assert all(float(r[4]) > 0 and float(r[5]) > 0 for r in rows[1:])
+    out = tmp_path / "cal.json"
+    assert main(["calibrate", "--bytes", str(1 << 24), "--repeats", "4", "--out", str(out)]) == 0
+    payload = json.loads(out.read_text())  # cli.py:356-363
+    assert payload["command"] == "calibrate" and payload["bytes"] == 1 << 24
+    assert len(payload["trial_times_s"]) == 4 and payload["mean_bytes_per_s"] > 0
+    assert main(["calibrate", "--bytes", "100"]) == 2
 
 
 def test_graphed_element_local_cg_bitwise(mesh3):
