@@ -6,11 +6,14 @@ OUT=${1:-gpurun_out/sanit}
 mkdir -p "$OUT"
 timeout 2000 compute-sanitizer --tool memcheck --leak-check no --error-exitcode 99 --print-limit 20 \
   python -m pytest tests/test_gpu_parity.py tests/test_gpu_helpers.py tests/test_gpu_assembly.py \
-  -q -x -p no:cacheprovider -k "not full_size and not sharded_assembled" > "$OUT/memcheck.log" 2>&1
+  tests/test_gpu_cg.py tests/test_gpu_acceptance.py -q -x -p no:cacheprovider \
+  -k "not full_size and not sharded_assembled and not 64bit and not two_ranks and not report_cli" \
+  > "$OUT/memcheck.log" 2>&1
 echo "exit $?" >> "$OUT/memcheck.log"
 timeout 2000 compute-sanitizer --tool racecheck --racecheck-report hazard --error-exitcode 99 \
-  --print-limit 20 python -m pytest tests/test_gpu_parity.py tests/test_gpu_helpers.py -q -x \
-  -p no:cacheprovider -k "degree_sweep or every_degree" > "$OUT/racecheck.log" 2>&1
+  --print-limit 20 python -m pytest tests/test_gpu_parity.py tests/test_gpu_helpers.py \
+  tests/test_gpu_assembly.py -q -x -p no:cacheprovider \
+  -k "degree_sweep or every_degree or golden or dss or cg_update" > "$OUT/racecheck.log" 2>&1
 echo "exit $?" >> "$OUT/racecheck.log"
 timeout 600 compute-sanitizer --tool synccheck --error-exitcode 99 python -m pytest \
   tests/test_gpu_parity.py -q -x -p no:cacheprovider -k "degree_sweep" > "$OUT/synccheck.log" 2>&1
