@@ -32,10 +32,6 @@
 #define HX_MINB_BP1_OF(N) Cfg<kBP1, N>::MINB
 #endif
 
-#ifndef HX_BP1_WREG
-#define HX_BP1_WREG 1  // S3's GwJ loaded into registers at tile start
-#endif
-
 namespace hx {
 
 template <int N>
@@ -125,7 +121,7 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT, HX_MINB_BP1_OF(N))
     // GwJ of this thread's S3 k-line, issued early so its latency hides
     // behind S1 and S2 (one-line-per-thread shapes only).
     double w[m];
-    if constexpr (ONE_C && HX_BP1_WREG) {
+    if constexpr (ONE_C) {
       const int el_c = tid / m2, ln_c = tid % m2;
       if (el_c < ne) {
         const double* g = p.gwj + (e0 + el_c) * fs + ln_c;
@@ -184,7 +180,7 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT, HX_MINB_BP1_OF(N))
       if (el >= ne) return;
       const int a = ln / m, c = ln % m;
       double wl[m];
-      if constexpr (ONE_C && HX_BP1_WREG) {
+      if constexpr (ONE_C) {
 #pragma unroll
         for (int t = 0; t < m; ++t) wl[t] = w[t];
       } else {
