@@ -32,13 +32,6 @@
 #define HX_MINB_BP1_OF(N) Cfg<kBP1, N>::MINB
 #endif
 
-#ifndef HX_BP1_WREG
-#define HX_BP1_WREG 1
-#endif
-#ifndef HX_BP1_QNEXT
-#define HX_BP1_QNEXT 1
-#endif
-
 namespace hx {
 
 template <int N>
@@ -112,26 +105,6 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT, HX_MINB_BP1_OF(N))
     prefetch_l2(p.gwj + e0 * fs, ne * fs * sizeof(double));
   }
 
-  // QN: a thread's S1 q line of the next tile is loaded into registers just
-  // before the tile's last barrier, where nothing else is live, so its L2
-  // latency overlaps the barrier wait instead of stalling S1.
-  constexpr bool QN = HX_BP1_QNEXT && !QST && EPB * n2 <= NT;
-  double xq[QN ? n : 1];
-  auto load_q = [&](int64_t t) {
-    if constexpr (QN) {
-      const int64_t f0 = t * EPB;
-      const int el = tid / n2, ln = tid % n2;
-      if (el < min64(EPB, p.n_el - f0)) {
-        int k, i;
-        line_coords<n, n, JKF>(ln, k, i);
-        const double* src = p.q + (f0 + el) * n3 + k * n2 + i;
-#pragma unroll
-        for (int t = 0; t < n; ++t) xq[t] = src[t * n];
-      }
-    }
-  };
-  if (blockIdx.x < ntiles) load_q(blockIdx.x);
-
   double en = 0.0;  // this thread's share of <q, A q> (ENERGY)
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t e0 = tile * EPB;
@@ -148,7 +121,7 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT, HX_MINB_BP1_OF(N))
     // GwJ of this thread's S3 k-line, issued early so its latency hides
     // behind S1 and S2 (one-line-per-thread shapes only).
     double w[m];
-    if constexpr (ONE_C && HX_BP1_WREG) {
+    if constexpr (ONE_C) {
       const int el_c = tid / m2, ln_c = tid % m2;
       if (el_c < ne) {
         const double* g = p.gwj + (e0 + el_c) * fs + ln_c;
@@ -169,7 +142,7 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT, HX_MINB_BP1_OF(N))
       const double* src = QST ? QT + (el * n + k) * QS + i : p.q + (e0 + el) * n3 + k * n2 + i;
       double x[n], y[m];
 #pragma unroll
-      for (int t = 0; t < n; ++t) x[t] = QN ? xq[t] : src[t * n];
+      for (int t = 0; t < n; ++t) x[t] = src[t * n];
       const bool bad = any_nonfinite(x);
       if (bad && p.flag) atomicOr(p.flag, 1);
       fold_apply<m, n, 1>(p.I, x, y);
@@ -207,7 +180,7 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT, HX_MINB_BP1_OF(N))
       if (el >= ne) return;
       const int a = ln / m, c = ln % m;
       double wl[m];
-      if constexpr (ONE_C && HX_BP1_WREG) {
+      if constexpr (ONE_C) {
 #pragma unroll
         for (int t = 0; t < m; ++t) wl[t] = w[t];
       } else {
@@ -262,7 +235,6 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT, HX_MINB_BP1_OF(N))
 #pragma unroll
       for (int t = 0; t < n; ++t) st_stream(dst + t * n, y[t]);
     });
-    if (tile + gridDim.x < ntiles) load_q(tile + gridDim.x);
     __syncthreads();  // X is rewritten by the next tile's S1
   }
   if constexpr (ENERGY) {
