@@ -1,6 +1,8 @@
 #!/usr/bin/env python3
 """Time the three N=7 BASELINE configs with whatever library HX_LIB_PATH
-points at (tuning experiments; prints one JSON line)."""
+points at (tuning experiments; prints one JSON line).  L2-warm; a GPU spacer
+before each timed launch keeps host launch latency out of small-E times
+(added after tune24: earlier BP1.0:16 entries include it)."""
 import json, os, statistics, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -17,6 +19,7 @@ def run(bp, side, deg=7, steps=30, warmup=5):
     ev = []
     for _ in range(steps):
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda._sleep(200_000)  # spacer: the launch is queued before `s` (bench.gpu_spacer)
         s.record(); hx.apply_device(op, q, out); e.record(); ev.append((s, e))
     torch.cuda.synchronize()
     ms = statistics.median(s.elapsed_time(e) for s, e in ev)
