@@ -312,6 +312,7 @@ int hx_apply_host(const hx_plan* Pc, const double* q_host, const double* factors
     if ((err = launch(*P, wq[slot], factors + e0 * P->elem_stride, wo[slot], ne, flag, s_k)) !=
         cudaSuccess) {
       cudaEventDestroy(start);
+      P->pipe_work = nullptr;  // the next call starts a fresh slot sequence
       return cuda_status(err);
     }
     cudaEventRecord(e_k[slot], s_k);
