@@ -291,6 +291,9 @@ int hx_apply_host(const hx_plan* Pc, const double* q_host, const double* factors
   const bool cont = P->pipe_work == work && P->pipe_chunk == chunk_el;
   if (!cont) {
     cudaStreamWaitEvent(s_in, start, 0);
+    // a previous call's pipeline may still be draining into the same
+    // workspace under another slot layout (or the caller switched streams)
+    if (P->pipe_seq > 0) cudaStreamWaitEvent(s_in, e_out[(P->pipe_seq - 1) % S], 0);
     P->pipe_seq = 0;
   }
   cudaStreamWaitEvent(s_k, start, 0);
@@ -313,6 +316,7 @@ int hx_apply_host(const hx_plan* Pc, const double* q_host, const double* factors
         cudaSuccess) {
       cudaEventDestroy(start);
       P->pipe_work = nullptr;  // the next call starts a fresh slot sequence
+      P->pipe_seq = g;         // ... after the chunks already queued
       return cuda_status(err);
     }
     cudaEventRecord(e_k[slot], s_k);
