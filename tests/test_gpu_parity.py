@@ -106,6 +106,27 @@ def test_host_path_bitwise_equals_device_path(bp, mesh3):
     np.testing.assert_array_equal(out, host.data)
 
 
+def test_host_pipeline_layout_and_stream_changes(mesh3):
+    """hx_apply_host back to back on one workspace with changing chunk sizes
+    (the slot layout changes under in-flight work) and changing streams:
+    every result is bitwise the device apply."""
+    op = hx.make_operator(hx.BP35, 7, mesh3, lam=1.0)
+    rng = np.random.default_rng(11)
+    qs = [torch.from_numpy(rng.standard_normal((op.n_el, op.n_p))).pin_memory()
+          for _ in range(6)]
+    outs = [torch.empty_like(q).pin_memory() for q in qs]
+    nbytes = _native.lib().hx_apply_host_workspace(op.plan.handle, 9)
+    work = torch.empty(nbytes // 8, dtype=torch.float64, device="cuda")
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    for i, (q, out) in enumerate(zip(qs, outs)):
+        st = streams[i % 2]
+        hx.apply_host(op, q.numpy(), out.numpy(), stream=st.cuda_stream,
+                      chunk_el=(9, 4, 4, 2, 9, 5)[i], work=work)
+    torch.cuda.synchronize()
+    for q, out in zip(qs, outs):
+        np.testing.assert_array_equal(out.numpy(), dev_apply(op, q.numpy()))
+
+
 def test_mass_volume_known_answers():
     """test_operators.py:68-78, test_acceptance.py:227-240 (conservation)."""
     cube = hx.build_cube_mesh(1, 2.0)
