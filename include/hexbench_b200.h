@@ -101,9 +101,10 @@ int hx_apply_range(const hx_plan* plan, const double* q, const double* factors, 
  * applied and copied back on a three-stream pipeline with three buffer slots,
  * so PCIe transfers in both directions overlap each other and the kernel.
  * Back-to-back calls with the same `work` and `chunk_el` continue the slot
- * sequence: the next call's H2D copies start while the previous call drains.  `work` is a device buffer of
- * at least hx_apply_host_workspace(plan, chunk_el) bytes; `stream` is made to
- * wait for the whole pipeline.                                              */
+ * sequence: the next call's H2D copies start while the previous call drains;
+ * a call with another `work` or `chunk_el` first waits for that drain.
+ * `work` is a device buffer of at least hx_apply_host_workspace(plan,
+ * chunk_el) bytes; `stream` is made to wait for the whole pipeline.          */
 int64_t hx_apply_host_workspace(const hx_plan* plan, int64_t chunk_el);
 int hx_apply_host(const hx_plan* plan, const double* q_host, const double* factors,
                   double* out_host, int64_t n_el, int64_t chunk_el, void* work,
