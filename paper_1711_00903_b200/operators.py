@@ -21,6 +21,7 @@ There is no CPU execution path: without the native library every apply
 raises ``NativeLibraryError``.
 """
 
+import threading
 from dataclasses import dataclass, field, fields
 
 import numpy as np
@@ -307,7 +308,7 @@ def _apply_host(op, src, dst, flag, stream, chunk_el=None, work=None):
 _STAGING_MIN_BYTES = 8 << 20
 _staging = {}
 _copy_pool = None
-_staging_lock = __import__("threading").Lock()  # one staging pair, one user at a time
+_staging_lock = threading.Lock()  # one staging pair, one user at a time
 
 
 def _parallel_copy(dst, src):
