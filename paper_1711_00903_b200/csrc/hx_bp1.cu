@@ -62,6 +62,11 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT, HX_MINB_BP1_OF(N))
   // a thread owns one line per stage when NT covers the tile's lines, else
   // it walks over several (small CTAs: cheap barriers, many CTAs per SM)
   constexpr bool ONE_C = EPB * m2 <= NT;
+  // W_LATE: S3's GwJ is loaded after S1, so its L2 latency hides behind the
+  // S1->S2 barrier and S2 instead of S1's q loads queueing behind it.  Faster
+  // at N = 7, 10, 13, 14 (tune26: N=7 config 1 with L2 warm 18.4 -> 16.4 us,
+  // E=32768 +1.5 %), slower at N = 1-4 and 9, where it costs registers.
+  constexpr bool W_LATE = N == 7 || N == 10 || N == 13 || N == 14;
   // QS > 0: the q tile is staged in shared memory by the bulk-copy engine
   // one tile ahead (k-slabs of n*n doubles at stride QS), so S1 never waits
   // on HBM; the q L2 prefetch is then not needed.
@@ -118,17 +123,18 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT, HX_MINB_BP1_OF(N))
         prefetch_l2(p.gwj + f0 * fs, nn * fs * sizeof(double));
       }
     }
-    // GwJ of this thread's S3 k-line, issued early so its latency hides
-    // behind S1 and S2 (one-line-per-thread shapes only).
+    // GwJ of this thread's S3 k-line (one-line-per-thread shapes), issued
+    // before S1 or, where that measured faster (W_LATE), after it
     double w[m];
-    if constexpr (ONE_C) {
+    auto load_w = [&]() {
       const int el_c = tid / m2, ln_c = tid % m2;
       if (el_c < ne) {
         const double* g = p.gwj + (e0 + el_c) * fs + ln_c;
 #pragma unroll
         for (int c = 0; c < m; ++c) w[c] = g[c * m2];
       }
-    }
+    };
+    if constexpr (ONE_C && !W_LATE) load_w();
     // ---- S1: j-lines (k, i): interpolate along s
     if constexpr (QST) {
       mbar_wait(qbar, qphase);
@@ -150,6 +156,7 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT, HX_MINB_BP1_OF(N))
 #pragma unroll
       for (int t = 0; t < m; ++t) dst[t * LX.s1] = y[t];
     });
+    if constexpr (ONE_C && W_LATE) load_w();
     __syncthreads();
     if constexpr (QST) {
       // the staged q has been consumed: fetch the next tile's into it
