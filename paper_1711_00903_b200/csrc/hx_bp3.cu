@@ -35,9 +35,6 @@
 #ifndef HX_BP3_REREAD_MIN_N
 #define HX_BP3_REREAD_MIN_N 7
 #endif
-#ifndef HX_BP3_RQT_SMEM
-#define HX_BP3_RQT_SMEM 0
-#endif
 #ifndef HX_PF_BP3
 #define HX_PF_BP3 2  // stage at which a tile's factors are prefetched into L2
 #endif
@@ -191,9 +188,6 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT, HX_MINB_BP3_OF(N))
       double* qsl = Bc + ca * LQS.s1 + cc;
       const double* g = p.fac + (e0 + el_c) * fs + ln_c;
       double rqt[m], tv[m], tt[m];
-      // RQT_SMEM: rqt goes through this thread's T line (re-read mode only)
-      constexpr bool RQT_SMEM = HX_BP3_RQT_SMEM && kReread;
-      double* const tl_w = Cc + ca * LT.s1 + cc;
       if constexpr (kReread) {
         // re-read this thread's own T k-line (still intact in C)
         const double* tl = Cc + ca * LT.s1 + cc;
@@ -218,20 +212,11 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT, HX_MINB_BP3_OF(N))
         const double rqs = grs * qr + gss * qs + gst * qt;
         qrl[LQR.kofs(t)] = rqr;
         qsl[LQS.kofs(t)] = rqs;
-        const double rt = grt * qr + gst * qs + gtt * qt;
-        if constexpr (RQT_SMEM) {
-          tl_w[LT.kofs(t)] = rt;  // this thread's own T k-line, already read
-        } else {
-          rqt[t] = rt;
-        }
+        rqt[t] = grt * qr + gst * qs + gtt * qt;
         const double lt = p.lam * gwj * tv[t];
         // <q, A q> = sum over GL points of grad t . G grad t + lam GwJ t^2
-        if constexpr (ENERGY) en += qr * rqr + qs * rqs + qt * rt + tv[t] * lt;
+        if constexpr (ENERGY) en += qr * rqr + qs * rqs + qt * rqt[t] + tv[t] * lt;
         tv[t] = lt;
-      }
-      if constexpr (RQT_SMEM) {
-#pragma unroll
-        for (int t = 0; t < m; ++t) rqt[t] = tl_w[LT.kofs(t)];
       }
       fold_apply<m, m, -1>(p.Dt, rqt, acc);
 #pragma unroll
