@@ -230,6 +230,36 @@ def test_non_finite_input_raises(perturbed_single):
         hx.apply_operator(op, hx.FieldVector(1, 125, bad))
 
 
+@pytest.mark.parametrize("bp", BPS)
+def test_non_finite_detected_in_every_position(bp, mesh3):
+    """A single inf / nan anywhere -- any element of a ragged batch, any node,
+    any chunk of the host pipeline -- sets the flag (operators.py:317-318);
+    a clean batch never does."""
+    op = hx.make_operator(bp, 3, mesh3, lam=0.5)
+    rng = np.random.default_rng(21)
+    q = rng.standard_normal((op.n_el, op.n_p))
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    qd = torch.from_numpy(q).cuda()
+    out = torch.empty_like(qd)
+    hx.apply_device(op, qd, out, flag)
+    out_h = np.empty_like(q)
+    hx.apply_host(op, q, out_h, flag, chunk_el=4)
+    torch.cuda.synchronize()
+    assert int(flag.item()) == 0
+    for e, node, val in ((0, 0, np.inf), (13, op.n_p // 2, np.nan), (op.n_el - 1, op.n_p - 1,
+                                                                       -np.inf)):
+        bad = q.copy()
+        bad[e, node] = val
+        for path in ("device", "host"):
+            flag.zero_()
+            if path == "device":
+                hx.apply_device(op, torch.from_numpy(bad).cuda(), out, flag)
+            else:
+                hx.apply_host(op, bad, out_h, flag, chunk_el=4)
+            torch.cuda.synchronize()
+            assert int(flag.item()) & 1, (e, node, path)
+
+
 def test_degenerate_geometry_raises():
     flat = hx.build_cube_mesh(1, 2.0).vertices.copy()
     flat[0, :, 2] = 0.0
