@@ -626,7 +626,7 @@ def run_ours(args):
     value = dofs_all / (ms_per_step * 1e-3) / 1e9
     achieved = bytes_per_apply / (kernel_ms * 1e-3) / 1e9
 
-    e2e_ms, e2e = e2e_report(op, mesh, max(3, args.steps // 4), 2)
+    e2e_ms, e2e = e2e_report(op, mesh, args.steps, max(3, args.warmup))  # same K as `value`
     e2e_ms = max_over_ranks(e2e_ms, world)
     e2e["value"] = dofs_all / (e2e_ms * 1e-3) / 1e9
     e2e["ms_per_step"] = e2e_ms
