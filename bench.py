@@ -11,8 +11,12 @@ BP1.0 config is timed with an L2 flush before every apply.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-Under torchrun each rank owns its own E-element shard (weak scaling, no
-data-path collective); the reported time is the max over ranks.
+With --gpus N > 1 and no torchrun environment, bench.py re-launches itself
+under torch.distributed.run with N ranks (one per GPU, NCCL).  Each rank owns
+its own E-element shard (weak scaling, no data-path collective); the
+reported time is the max over ranks.  The JSON line ends with the compact
+per-config ``per_bp`` table; the full secondary legs (CG, unfused baseline,
+calibrations, host paths) go to gpurun_out/bench_details.json.
 """
 
 import argparse
@@ -34,7 +38,10 @@ DEGREE = 7
 LAM = 1.0
 HEADLINE = ("BP3.5", 32)          # configs[1]: side 32 -> E = 32768
 EXTRA = (("BP1.0", 16), ("BP3.0", 32), ("BP1.0", 32))
-SAMPLE_EL = 2048                  # CPU-baseline sample (elements)
+SAMPLE_EL = 2048                  # CPU-baseline sample of the oracle port (elements)
+REF_SAMPLE_EL = 512               # ... of the reference itself (0.15 s per BP3.5 apply)
+REF_PATH = os.path.join(ROOT, "baseline", "_ref")  # pip-installed reference (hexbench)
+DETAILS = os.path.join(ROOT, "gpurun_out", "bench_details.json")
 
 
 def load_peaks():
@@ -154,12 +161,18 @@ def dist_setup(args):
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: launch one "
+                         "rank per GPU (bench.py re-launches itself when WORLD_SIZE is unset)")
     # one rank per GPU; HX_BENCH_BACKEND=gloo (test only) lets several ranks
     # share one GPU to exercise the multi-rank code paths on a one-GPU box
-    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
+    backend = os.environ.get("HX_BENCH_BACKEND", "nccl")
+    ndev = torch.cuda.device_count()
+    if world > 1 and backend == "nccl" and world > ndev:
+        raise SystemExit(f"bench.py: {world} NCCL ranks need {world} GPUs, this node has {ndev}")
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, ndev)
     if world > 1:
         torch.cuda.set_device(local)
-        backend = os.environ.get("HX_BENCH_BACKEND", "nccl")
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
@@ -167,6 +180,25 @@ def dist_setup(args):
     else:
         torch.cuda.set_device(0)
     return rank, world, local
+
+
+def relaunch(args):
+    """--gpus N > 1 outside torchrun: run this script under
+    torch.distributed.run with N ranks on this node (one per GPU, NCCL with
+    its INIT log on so the communicator's N ranks are visible) and exit with
+    its status.  Only rank 0 prints the JSON line."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    sys.exit(subprocess.call(cmd, env=env))
 
 
 def _reduce_device():
@@ -308,7 +340,7 @@ def bp_report(bp, side, rank, steps, warmup, hbm_peak):
     return rep
 
 
-def cpu_baseline(bp=HEADLINE[0]):
+def port_cpu(sample_el=SAMPLE_EL, bp=HEADLINE[0], seconds=5.0):
     """Oracle port (numpy restatement of the reference apply) on a bounded
     sample of the headline workload, BLAS pinned to one thread."""
     import paper_1711_00903_b200 as hx
@@ -319,12 +351,12 @@ def cpu_baseline(bp=HEADLINE[0]):
         threadpool_limits = None
 
     mesh = hx.perturb_mesh(hx.build_cube_mesh(HEADLINE[1], 2.0), amplitude=0.15, seed=7)
-    sub = hx.HexMesh(SAMPLE_EL, mesh.vertices[:SAMPLE_EL], mesh.extent)
-    op = hx.make_operator(bp, DEGREE, sub, lam=LAM)
-    fac = op.factors.data
-    q = np.random.default_rng(0).standard_normal((SAMPLE_EL, op.n_p))
-    interp = None if op.interp is None else op.interp.entries
-    diff = None if op.diff is None else op.diff.entries
+    sub = hx.HexMesh(sample_el, mesh.vertices[:sample_el], mesh.extent)
+    rule = hx.gll_rule(DEGREE + 1) if bp == "BP3.5" else hx.gl_rule(DEGREE + 2)
+    fac = hx.geometric_factors(sub, rule).data
+    q = np.random.default_rng(0).standard_normal((sample_el, (DEGREE + 1) ** 3))
+    interp = hx.interp_matrix(DEGREE).entries
+    diff = (hx.diff_matrix_gll if bp == "BP3.5" else hx.diff_matrix_gl)(DEGREE).entries
     ctx = threadpool_limits(1) if threadpool_limits else None
     if ctx:
         ctx.__enter__()
@@ -335,40 +367,101 @@ def cpu_baseline(bp=HEADLINE[0]):
             orc.apply_chunked(bp, DEGREE, LAM, interp, diff, fac, q)
             reps += 1
             el = time.perf_counter() - t0
-            if el > 10.0 or reps >= 200:
+            if el > seconds or reps >= 200:
                 break
     finally:
         if ctx:
             ctx.__exit__(None, None, None)
-    per = el / reps
-    return {"value": SAMPLE_EL * op.n_p / per / 1e9, "unit": "GDOF/s", "cores": 1,
+    return {"value": sample_el * q.shape[1] / (el / reps) / 1e9, "unit": "GDOF/s", "cores": 1,
             "kind": "port",
-            "sample": f"{bp} N={DEGREE} first {SAMPLE_EL} elements of the E=32768 mesh, "
+            "sample": f"{bp} N={DEGREE} first {sample_el} elements of the E=32768 mesh, "
                       f"{reps} applies in {el:.1f} s (oracle/hexbench_oracle.py, numpy, "
                       "1 BLAS thread)"}
 
 
-E2E_CHUNK_BYTES = 64 << 20
+def reference_available():
+    return os.path.isdir(os.path.join(REF_PATH, "hexbench"))
+
+
+class ReferenceWorkload:
+    """The unmodified reference package (pip-installed into baseline/_ref by
+    tools/install_reference.sh) on a bounded sample of the headline mesh:
+    its own HexMesh / make_operator / FieldVector / apply_operator
+    (operators.py:118-143, :306-331), threads = the reference's own
+    element-range thread pool.  The sample's corners are the first
+    `sample_el` elements of perturb_mesh(build_cube_mesh(32, 2.0), 0.15,
+    seed=7) -- built with this package's mesh module, which reproduces the
+    reference's bit for bit (tests/test_oracle_golden.py), because the
+    reference's own perturb_mesh of all 32768 elements alone takes minutes."""
+
+    def __init__(self, sample_el, bp=HEADLINE[0]):
+        import paper_1711_00903_b200 as hx
+        if REF_PATH not in sys.path:
+            sys.path.insert(0, REF_PATH)
+        from hexbench import mesh as rmesh
+        from hexbench import operators as rops
+        full = hx.perturb_mesh(hx.build_cube_mesh(HEADLINE[1], 2.0), amplitude=0.15, seed=7)
+        sub = rmesh.HexMesh(sample_el, np.array(full.vertices[:sample_el]), full.extent)
+        self.rops = rops
+        self.bp, self.sample_el = bp, sample_el
+        self.op = rops.make_operator(bp, DEGREE, sub, lam=LAM)
+        self.q = rops.FieldVector.random(sample_el, self.op.n_p, seed=0)
+        self.dofs = sample_el * self.op.n_p
+
+    def step(self, threads):
+        self.rops.apply_operator(self.op, self.q, threads=threads)
+
+    def rate(self, threads, seconds=3.0, min_reps=2):
+        self.step(threads)  # warm-up
+        reps, t0 = 0, time.perf_counter()
+        while True:
+            self.step(threads)
+            reps += 1
+            el = time.perf_counter() - t0
+            if el > seconds and reps >= min_reps:
+                break
+        return self.dofs / (el / reps) / 1e9, reps, el
+
+
+def reference_cpu(seconds=3.0):
+    """cpu_baseline of our arm: the reference itself at threads=1 and
+    threads=<host cores> on REF_SAMPLE_EL elements, plus the oracle port
+    (one core).  Falls back to the port alone without baseline/_ref."""
+    port = port_cpu(seconds=seconds)
+    if not reference_available():
+        port["note"] = "baseline/_ref missing: oracle port only"
+        return port
+    cores = os.cpu_count() or 1
+    w = ReferenceWorkload(REF_SAMPLE_EL)
+    v1, r1, e1 = w.rate(1, seconds)
+    vt, rt, et = w.rate(cores, seconds)
+    best_threads, best = (cores, vt) if vt >= v1 else (1, v1)
+    return {"value": best, "unit": "GDOF/s", "cores": best_threads, "kind": "reference",
+            "sample": f"{w.bp} N={DEGREE}: first {REF_SAMPLE_EL} elements of the E=32768 mesh "
+                      "through the unmodified reference apply_operator (baseline/_ref); value = "
+                      "the faster of threads=1 / threads=cores",
+            "threads_1": {"value": v1, "cores": 1, "applies": r1, "seconds": round(e1, 2)},
+            f"threads_{cores}": {"value": vt, "cores": cores, "applies": rt,
+                                 "seconds": round(et, 2)},
+            "port": {k: port[k] for k in ("value", "cores", "kind", "sample")}}
 
 
 def e2e_report(op, mesh, steps, warmup):
-    """Same metric through the public host-buffer API (hx_apply_host): per step
-    the H2D copy of q from pinned memory, the kernel and the D2H copy of out."""
+    """Same metric through the public host-buffer API (hx_apply_host, the
+    library's default chunking): per step the H2D copy of q from pinned
+    memory, the kernel and the D2H copy of out, each call stream-ordered
+    after the previous one (no cross-call overlap)."""
     import torch
     import paper_1711_00903_b200 as hx
+    from paper_1711_00903_b200 import operators
 
     n = mesh.n_el * op.n_p
     q_pin = torch.empty(n, dtype=torch.float64).pin_memory()
     q_pin.copy_(torch.from_numpy(np.random.default_rng(0).standard_normal(n)))
     o_pin = torch.empty(n, dtype=torch.float64).pin_memory()
     qh, oh = q_pin.numpy(), o_pin.numpy()
-    # back-to-back steps keep the pipeline full across calls, where uniform
-    # 64 MiB chunks beat the library default (32 MiB with ramped ends, tuned
-    # for isolated calls): 2.84-2.90 vs 3.02 ms per step (profiles/tuning tune28)
-    chunk = hx.operators.host_chunk_elements(op, E2E_CHUNK_BYTES)
-    from paper_1711_00903_b200 import _native
-    nbytes = _native.lib().hx_apply_host_workspace(op.plan.handle, chunk)
-    work = torch.empty(nbytes // 8, dtype=torch.float64, device="cuda")
+    chunk = operators.host_chunk_elements(op)
+    work = operators._device_work(op, chunk)
     stream = torch.cuda.current_stream()
     for _ in range(warmup):
         hx.apply_host(op, qh, oh, chunk_el=chunk, work=work)
@@ -383,7 +476,33 @@ def e2e_report(op, mesh, steps, warmup):
     return ms, {"value": None, "unit": "GDOF/s", "h2d_bytes_per_step": n * 8,
                 "d2h_bytes_per_step": n * 8, "ms_per_step": ms,
                 "path": "hx_apply_host (C ABI), pinned host q/out, chunked 3-stream "
-                        f"H2D/kernel/D2H pipeline, chunk {chunk} elements"}
+                        f"H2D/kernel/D2H pipeline, chunk {chunk} elements, stream-ordered calls"}
+
+
+def e2e_api_report(op, mesh, steps, warmup):
+    """The call a reference user makes: apply_operator(op, FieldVector(numpy))
+    on a plain pageable numpy array (reference operators.py:306), through
+    hx_apply_host_staged; host-synchronous, timed by wall clock per call."""
+    import torch
+    import paper_1711_00903_b200 as hx
+
+    fv = hx.FieldVector(mesh.n_el, op.n_p,
+                        np.random.default_rng(0).standard_normal((mesh.n_el, op.n_p)))
+    for _ in range(warmup):
+        hx.apply_operator(op, fv)
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        out = hx.apply_operator(op, fv)
+        ts.append(time.perf_counter() - t0)
+        del out
+    ms = statistics.median(ts) * 1e3
+    return {"value": mesh.n_el * op.n_p / (ms * 1e-3) / 1e9, "unit": "GDOF/s",
+            "ms_per_step": ms, "h2d_bytes_per_step": fv.data.nbytes,
+            "d2h_bytes_per_step": fv.data.nbytes,
+            "path": "apply_operator(op, FieldVector(pageable numpy)) -> hx_apply_host_staged "
+                    "(pinned staging ring, host copy threads), median wall clock"}
 
 
 def pcie_bandwidth(nbytes, trials=5):
@@ -585,6 +704,37 @@ def baseline_report(steps=5, warmup=2, side=32):
     return res
 
 
+def kernel_profile(bp):
+    """Per-launch counters of the kernel from the committed ncu capture
+    (profiles/kernels.json, written by tools/ncu_summary.py), per element."""
+    path = os.path.join(ROOT, "profiles", "kernels.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as fh:
+        k = json.load(fh).get(f"{KERNEL[bp]}<{DEGREE}>")
+    return k
+
+
+KERNEL = {"BP1.0": "bp1_kernel", "BP3.5": "bp35_kernel", "BP3.0": "bp3_kernel"}
+SMEM_WAVEFRONT_BYTES = 128  # one shared-memory wavefront: 32 banks x 4 B per cycle
+
+
+def smem_roofline(rep, b_smem):
+    """Shared-memory roofline of one per_bp entry: the kernel's measured
+    shared-memory wavefronts per element (ncu) x 128 B, over the kernel time,
+    against the measured LDS bandwidth (north_star (4); the paper's B_sh,
+    PAPER.md:476-487)."""
+    k = kernel_profile(rep["bp"])
+    if not k or not b_smem:
+        return None
+    wf = k["smem_wavefronts"] / k["n_el"]
+    nbytes = wf * SMEM_WAVEFRONT_BYTES * rep["n_el"]
+    achieved = nbytes / (rep["kernel_ms_median"] * 1e-3)
+    return {"smem_bytes_per_element": wf * SMEM_WAVEFRONT_BYTES,
+            "smem_gb_per_s": achieved / 1e9, "smem_roofline_frac": achieved / b_smem,
+            "ncu": k.get("source")}
+
+
 def run_ours(args):
     import torch
     import paper_1711_00903_b200 as hx
@@ -626,46 +776,59 @@ def run_ours(args):
     value = dofs_all / (ms_per_step * 1e-3) / 1e9
     achieved = bytes_per_apply / (kernel_ms * 1e-3) / 1e9
 
+    barrier(world)
     e2e_ms, e2e = e2e_report(op, mesh, args.steps, max(3, args.warmup))  # same K as `value`
     e2e_ms = max_over_ranks(e2e_ms, world)
     e2e["value"] = dofs_all / (e2e_ms * 1e-3) / 1e9
     e2e["ms_per_step"] = e2e_ms
-    if rank == 0 and not args.quick:
+    full = rank == 0 and not args.quick
+    details = {}
+    if full:
         pcie = pcie_bandwidth(e2e["h2d_bytes_per_step"])
-        e2e["pcie"] = pcie
+        details["pcie"] = pcie
         e2e["frac_of_pcie_bound"] = pcie["bidirectional_ms"] / e2e_ms
-    cg = cg_report(op, mesh) if (rank == 0 and not args.quick) else None
-    cg_asm = cg_assembled_report() if (rank == 0 and not args.quick) else None
-    unfused = baseline_report() if (rank == 0 and not args.quick) else None
-    calib = None
-    if rank == 0 and not args.quick:
+        api = e2e_api_report(op, mesh, args.steps, max(3, args.warmup))
+        api["vs_pinned_e2e"] = api["ms_per_step"] / e2e_ms
+        e2e["api"] = {k: api[k] for k in ("value", "ms_per_step", "vs_pinned_e2e")}
+        details["e2e_api"] = api
+    b_smem = None
+    if full:
         import ctypes
         from paper_1711_00903_b200 import _native
         bsh = ctypes.c_double()
         _native.check(_native.lib().hx_measure_smem_bandwidth(
             ctypes.byref(bsh), torch.cuda.current_stream().cuda_stream))
-        calib = {"b_smem_measured_gb_per_s": bsh.value / 1e9,
-                 "b_smem_paper_ansatz_gb_per_s": hx.shared_bandwidth_ansatz(
-                     148, 32, 4, 1.965) / 1e9,
-                 "note": "measured LDS.64 bandwidth (hx_measure_smem_bandwidth) replaces "
-                         "the paper's B_sh ansatz (PAPER.md:476-487)"}
+        b_smem = bsh.value
+        details["calibration"] = {
+            "b_smem_measured_gb_per_s": b_smem / 1e9,
+            "b_smem_paper_ansatz_gb_per_s": hx.shared_bandwidth_ansatz(148, 32, 4, 1.965) / 1e9,
+            "note": "measured LDS.64 bandwidth (hx_measure_smem_bandwidth) replaces the "
+                    "paper's B_sh ansatz (PAPER.md:476-487)"}
+        details["cg"] = cg_report(op, mesh)
+        details["cg_assembled"] = cg_assembled_report()
+        details["unfused_baseline"] = baseline_report()
 
     traffic = None
-    tpath = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tpath):
-        with open(tpath) as fh:
-            traffic = json.load(fh).get("bp35_kernel<7>")
+    prof = kernel_profile(bp)
+    if prof:
+        traffic = prof["dram_bytes"] / prof["n_el"] * mesh.n_el
 
     per_bp = {}
     cpu = None
     del op, q, out
     torch.cuda.empty_cache()
-    if rank == 0 and world == 1 and not args.quick:
-        per_bp[f"{bp} E={mesh.n_el}"] = bp_report(bp, side, 0, args.steps, args.warmup, hbm_peak)
-        for xbp, xside in EXTRA:
+    if full and world == 1:
+        for xbp, xside in ((bp, side),) + EXTRA:
             r = bp_report(xbp, xside, 0, args.steps, args.warmup, hbm_peak)
-            per_bp[f"{xbp} E={r['n_el']}"] = r
-        cpu = cpu_baseline()
+            sm = smem_roofline(r, b_smem)
+            if sm:
+                r.update(sm)
+            details.setdefault("per_bp", {})[f"{xbp} E={r['n_el']}"] = r
+            per_bp[f"{xbp} E={r['n_el']}"] = {
+                k: (round(r[k], 4) if isinstance(r.get(k), float) else r.get(k))
+                for k in ("gdof_per_s", "frac_of_measured_peak", "frac_of_copy_same_size",
+                          "kernel_ms_median", "smem_roofline_frac")}
+        cpu = reference_cpu()
 
     if rank == 0:
         line = {
@@ -687,23 +850,37 @@ def run_ours(args):
             "gpu_launches": args.steps,
             "clocks": clocks.summary(),
             "cpu_baseline": cpu,
-            "per_bp": per_bp,
-            "cg": cg,
-            "cg_assembled": cg_asm,
-            "unfused_baseline": unfused,
-            "calibration": calib,
             "gflop_per_s": hx.flop_model(bp, "fused", DEGREE) * dofs_all / (DEGREE + 1) ** 3
                            / (ms_per_step * 1e-3) / 1e9,
         }
+        if details:
+            line["details"] = summarize_details(details)
+            os.makedirs(os.path.dirname(DETAILS), exist_ok=True)
+            with open(DETAILS, "w") as fh:
+                json.dump(details, fh, indent=1)
+        line["per_bp"] = per_bp  # last: the driver keeps the tail of the line
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
 
 
-# ---------------------------------------------------------------------------
-# reference arm: the oracle port on the host cores
-# ---------------------------------------------------------------------------
+def summarize_details(d):
+    """A few headline numbers of the secondary legs for the JSON line (the
+    full legs are in gpurun_out/bench_details.json)."""
+    out = {"file": os.path.relpath(DETAILS, ROOT)}
+    if "calibration" in d:
+        out["b_smem_gb_per_s"] = round(d["calibration"]["b_smem_measured_gb_per_s"], 1)
+    if "cg" in d:
+        out["cg_ms_per_iteration"] = round(d["cg"]["ms_per_iteration"], 4)
+    if "cg_assembled" in d:
+        out["cg_assembled_ms_per_iteration"] = round(d["cg_assembled"]["ms_per_iteration"], 4)
+    if "unfused_baseline" in d:
+        out["fused_speedup_over_unfused"] = {
+            k: round(v["speedup_fused_over_baseline"], 2)
+            for k, v in d["unfused_baseline"].items()}
+    return out
+
 
 def arm_config(bp, n_el, world):
     """The `config` both arms report (same workload, same keys)."""
@@ -714,40 +891,73 @@ def arm_config(bp, n_el, world):
 
 
 def run_reference(args):
-    """The reference arm: the reference's own CPU algorithm for the path (the
-    oracle port -- the reference is pure Python/numpy and does not travel to
-    the GPU box) on all host cores, rank 0 only."""
+    """The reference arm: the reference's own CPU implementation of the path
+    -- the unmodified hexbench package pip-installed into baseline/_ref --
+    through its public apply_operator with its element-range thread pool on
+    all host cores, each step a bounded sample of the headline workload;
+    rank 0 only.  Without baseline/_ref: the oracle port, threads over
+    element ranges."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    cores = os.cpu_count() or 1
+    bp = HEADLINE[0]
+    if reference_available():
+        sample = 1024
+        w = ReferenceWorkload(sample)
+        for _ in range(args.warmup):
+            w.step(cores)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            w.step(cores)
+        el = time.perf_counter() - t0
+        ms = el / args.steps * 1e3
+        value = w.dofs / (ms * 1e-3) / 1e9
+        kind = "reference"
+        desc = (f"bounded sample: first {sample} of the 32768 elements per step through the "
+                "unmodified reference apply_operator(op, q, threads=" + str(cores) + ") "
+                "(baseline/_ref, hexbench 0.1.0)")
+    else:
+        value, ms, desc = port_reference_steps(args, cores)
+        kind = "port"
+    line = {
+        "metric": METRIC, "value": value, "unit": "GDOF/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "impl": "reference",
+        "data": "synthetic: same mesh / q generator as the GPU arm",
+        "config": arm_config(bp, HEADLINE[1] ** 3, 1),
+        "cpu_baseline": {"value": value, "unit": "GDOF/s", "cores": cores, "kind": kind,
+                         "sample": desc},
+        "e2e": {"value": value, "unit": "GDOF/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def port_reference_steps(args, cores):
+    """Fallback reference arm: the oracle port on all host cores (4096-element
+    sample per step, one BLAS thread per worker thread)."""
     from concurrent.futures import ThreadPoolExecutor
 
     import paper_1711_00903_b200 as hx
     from oracle import hexbench_oracle as orc
 
     bp, side = HEADLINE
-    cores = os.cpu_count() or 1
     sample = 4096
     mesh = hx.perturb_mesh(hx.build_cube_mesh(side, 2.0), amplitude=0.15, seed=7)
     sub = hx.HexMesh(sample, mesh.vertices[:sample], mesh.extent)
-    fac = hx.geometric_factors(sub, hx.gll_rule(DEGREE + 1) if bp == "BP3.5"
-                               else hx.gl_rule(DEGREE + 2)).data
+    fac = hx.geometric_factors(sub, hx.gll_rule(DEGREE + 1)).data
     diff = hx.diff_matrix_gll(DEGREE).entries
     q = np.random.default_rng(0).standard_normal((sample, (DEGREE + 1) ** 3))
     chunks = np.linspace(0, sample, cores + 1).astype(int)
-
-    def work(rng):
-        lo, hi = rng
-        return orc.apply(bp, DEGREE, LAM, None, diff, fac[lo:hi], q[lo:hi])
-
-    pool = ThreadPoolExecutor(max_workers=cores)
     spans = [(lo, hi) for lo, hi in zip(chunks[:-1], chunks[1:]) if hi > lo]
+    pool = ThreadPoolExecutor(max_workers=cores)
 
     def step():
-        list(pool.map(work, spans))
+        list(pool.map(lambda r: orc.apply(bp, DEGREE, LAM, None, diff, fac[r[0]:r[1]],
+                                          q[r[0]:r[1]]), spans))
 
-    # one BLAS thread per worker thread: `cores` threads in total, no
-    # oversubscription (numpy releases the GIL inside the BLAS calls)
     import contextlib
     try:
         from threadpoolctl import threadpool_limits
@@ -762,22 +972,9 @@ def run_reference(args):
             step()
         el = time.perf_counter() - t0
     ms = el / args.steps * 1e3
-    value = sample * q.shape[1] / (ms * 1e-3) / 1e9
-    line = {
-        "metric": METRIC, "value": value, "unit": "GDOF/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "impl": "reference",
-        "data": "synthetic: same mesh / q generator as the GPU arm",
-        "config": arm_config(bp, mesh.n_el, 1),
-        "cpu_baseline": {"value": value, "unit": "GDOF/s", "cores": cores, "kind": "port",
-                         "sample": f"bounded sample: first {sample} of the {mesh.n_el} "
-                                   f"elements per step, {cores} threads over element ranges "
-                                   "(1 BLAS thread each), oracle/hexbench_oracle.py (numpy)"},
-        "e2e": {"value": value, "unit": "GDOF/s", "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": 0},
-    }
-    print(json.dumps(line), flush=True)
+    return (sample * q.shape[1] / (ms * 1e-3) / 1e9, ms,
+            f"bounded sample: first {sample} of the {mesh.n_el} elements per step, {cores} "
+            "threads over element ranges (1 BLAS thread each), oracle/hexbench_oracle.py")
 
 
 def main():
@@ -791,6 +988,10 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus < 1:
+        raise SystemExit("--gpus must be >= 1")
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch(args)
     if args.impl == "reference":
         run_reference(args)
     else:

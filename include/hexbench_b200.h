@@ -100,15 +100,44 @@ int hx_apply_range(const hx_plan* plan, const double* q, const double* factors, 
  * up to `chunk_el` elements (ramped up and down at the ends) are copied in,
  * applied and copied back on a three-stream pipeline with three buffer slots,
  * so PCIe transfers in both directions overlap each other and the kernel.
- * Back-to-back calls with the same `work` and `chunk_el` continue the slot
- * sequence: the next call's H2D copies start while the previous call drains;
- * a call with another `work` or `chunk_el` first waits for that drain.
- * `work` is a device buffer of at least hx_apply_host_workspace(plan,
- * chunk_el) bytes; `stream` is made to wait for the whole pipeline.          */
+ * Stream-ordered like hx_apply: the pipeline starts after everything queued
+ * on `stream` before the call (so q_host may be produced by earlier work on
+ * `stream`, e.g. a previous call's D2H), and `stream` is made to wait for the
+ * whole pipeline.  `work` is a device buffer of at least
+ * hx_apply_host_workspace(plan, chunk_el) bytes, used under the same stream
+ * order.  The pipeline streams live on the device current at the call (they
+ * are rebuilt if a plan moves to another device).  On an error return no copy
+ * into or out of the host buffers is still in flight.                        */
 int64_t hx_apply_host_workspace(const hx_plan* plan, int64_t chunk_el);
 int hx_apply_host(const hx_plan* plan, const double* q_host, const double* factors,
                   double* out_host, int64_t n_el, int64_t chunk_el, void* work,
                   int* status_flag, void* stream);
+
+/* Drop-in host path for the arrays the reference's users pass to
+ * apply_operator (operators.py:306-331): q_host / out_host may be PAGEABLE
+ * (plain numpy memory).  Pageable buffers stream through `staging`, a
+ * page-locked host buffer of hx_apply_host_staging_bytes(plan, chunk_el)
+ * bytes: host worker threads copy chunk c+1 of q into a pinned slot while
+ * chunk c is on PCIe / in the kernel, and copy finished chunks of out back
+ * while later ones run; page-locked q_host / out_host skip their staging.
+ * Same device pipeline and `work` buffer as hx_apply_host, same stream order;
+ * HOST-SYNCHRONOUS: returns once out_host holds the result (or on error,
+ * with no copy touching the host buffers still in flight).  Worker threads:
+ * hardware concurrency, or HX_HOST_THREADS.                                  */
+int64_t hx_apply_host_staging_bytes(const hx_plan* plan, int64_t chunk_el);
+int hx_apply_host_staged(const hx_plan* plan, const double* q_host, const double* factors,
+                         double* out_host, int64_t n_el, int64_t chunk_el, void* work,
+                         void* staging, int* status_flag, void* stream);
+
+/* The reference's up-front non-finite scan (operators.py:317-318), for
+ * callers that must not have an output buffer touched on bad input (the
+ * applies themselves fuse the same test into their loads):
+ *   hx_check_finite   : device x[0, n); ORs HX_FLAG_NONFINITE into the device
+ *                       int *status_flag (asynchronous on `stream`)
+ *   hx_host_all_finite: host x[0, n) scanned by the host worker threads;
+ *                       returns 1 if every entry is finite, else 0           */
+int hx_check_finite(const double* x, int64_t n, int* status_flag, void* stream);
+int hx_host_all_finite(const double* x, int64_t n);
 
 /* Unfused "baseline" apply: the paper's Kernel-1 structure and
  * the reference's variant="baseline" access pattern (operators.py:170-200):
@@ -127,7 +156,11 @@ int hx_apply_baseline(const hx_plan* plan, const double* q, const double* factor
  * tensors, (k,j,i) point order:
  *   project = 0: dst (n_el, m^3) = I (x) I (x) I  src (n_el, n^3)
  *   project = 1: dst (n_el, n^3) = I^T (x) I^T (x) I^T  src (n_el, m^3)
- * status_flag as in hx_apply (non-finite src).  Asynchronous on `stream`.    */
+ * status_flag as in hx_apply (non-finite src).  Asynchronous on `stream`.
+ * Centro-symmetric matrices (every GLL->GL interpolation matrix) take the
+ * folded fused kernel; any other finite matrix takes unfused dense passes
+ * with stream-ordered scratch (cudaMallocAsync), like the reference's
+ * contract_dim, which accepts any 2-D matrix.                                */
 int hx_interp_elements(int degree, const double* interp, int project, const double* src,
                        double* dst, int64_t n_el, int* status_flag, void* stream);
 

@@ -34,6 +34,11 @@ SIGNATURES = {
     "hx_apply_range": (_c.c_int, [_P, _P, _P, _P, _c.c_int64, _c.c_int64, _P, _P]),
     "hx_apply_host_workspace": (_c.c_int64, [_P, _c.c_int64]),
     "hx_apply_host": (_c.c_int, [_P, _P, _P, _P, _c.c_int64, _c.c_int64, _P, _P, _P]),
+    "hx_apply_host_staging_bytes": (_c.c_int64, [_P, _c.c_int64]),
+    "hx_apply_host_staged": (_c.c_int, [_P, _P, _P, _P, _c.c_int64, _c.c_int64, _P, _P, _P,
+                                        _P]),
+    "hx_check_finite": (_c.c_int, [_P, _c.c_int64, _P, _P]),
+    "hx_host_all_finite": (_c.c_int, [_P, _c.c_int64]),
     "hx_plan_kernel_shape": (_c.c_int, [_P, _c.POINTER(_c.c_int), _c.POINTER(_c.c_int),
                                         _c.POINTER(_c.c_int)]),
     "hx_measure_smem_bandwidth": (_c.c_int, [_c.POINTER(_c.c_double), _P]),

@@ -195,6 +195,38 @@ static cudaError_t baseline_n(const hx_plan& P, const double* q, const double* f
   return project3<n, m>(P.interp, w3, w0, w1, out, E, s);
 }
 
+// Dense (unfolded) element interpolation / projection for 1-D matrices the
+// folded kernels cannot take (not centro-symmetric): the reference's
+// contract_dim passes (operators.py:352-364) as line passes, intermediates in
+// stream-ordered scratch.  Not a hot path.
+template <int N>
+static cudaError_t interp_dense_n(const double* I, int project, const double* src, double* dst,
+                                  int64_t E, cudaStream_t s) {
+  constexpr int n = N + 1, m = N + 2;
+  const int64_t a = project ? m * n * m : n * m * n, b = project ? m * n * n : n * m * m;
+  double* w = nullptr;
+  HX_TRY(cudaMallocAsync(reinterpret_cast<void**>(&w), sizeof(double) * (a + b) * E, s));
+  const cudaError_t err = project ? project3<n, m>(I, src, w, w + a * E, dst, E, s)
+                                  : interp3<n, m>(I, src, w, w + a * E, dst, E, s);
+  const cudaError_t fr = cudaFreeAsync(w, s);
+  return err != cudaSuccess ? err : fr;
+}
+
+cudaError_t launch_interp_dense(int degree, const double* interp, int project, const double* src,
+                                double* dst, int64_t n_el, cudaStream_t s) {
+  if (n_el == 0) return cudaSuccess;
+  switch (degree) {
+#define HX_CASE(N) \
+  case N:          \
+    return interp_dense_n<N>(interp, project, src, dst, n_el, s);
+    HX_CASE(1) HX_CASE(2) HX_CASE(3) HX_CASE(4) HX_CASE(5) HX_CASE(6) HX_CASE(7) HX_CASE(8)
+    HX_CASE(9) HX_CASE(10) HX_CASE(11) HX_CASE(12) HX_CASE(13) HX_CASE(14) HX_CASE(15)
+#undef HX_CASE
+    default:
+      return cudaErrorInvalidValue;
+  }
+}
+
 int64_t baseline_workspace_doubles(const hx_plan& P, int64_t n_el) {
   return 4 * n_el * int64_t(P.m) * P.m * P.m;
 }

@@ -145,10 +145,18 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT, HX_MINB_BP1_OF(N))
       if (el >= ne) return;
       int k, i;
       line_coords<n, n, JKF>(ln, k, i);
+#ifdef HX_EXP_COAL
+      // EXPERIMENT (wrong numerics): k-line addressing, coalesced 256 B per warp
+      const double* src = p.q + (e0 + el) * n3 + ln;
+      double x[n], y[m];
+#pragma unroll
+      for (int t = 0; t < n; ++t) x[t] = src[t * n2];
+#else
       const double* src = QST ? QT + (el * n + k) * QS + i : p.q + (e0 + el) * n3 + k * n2 + i;
       double x[n], y[m];
 #pragma unroll
       for (int t = 0; t < n; ++t) x[t] = src[t * n];
+#endif
       const bool bad = any_nonfinite(x);
       if (bad && p.flag) atomicOr(p.flag, 1);
       fold_apply<m, n, 1>(p.I, x, y);
@@ -238,9 +246,15 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT, HX_MINB_BP1_OF(N))
 #pragma unroll
       for (int t = 0; t < m; ++t) x[t] = src[t * LX.s1];
       fold_apply<n, m, 1>(p.It, x, y);
+#ifdef HX_EXP_COAL
+      double* dst = p.out + (e0 + el) * n3 + ln;
+#pragma unroll
+      for (int t = 0; t < n; ++t) st_stream(dst + t * n2, y[t]);
+#else
       double* dst = p.out + (e0 + el) * n3 + k * n2 + i;
 #pragma unroll
       for (int t = 0; t < n; ++t) st_stream(dst + t * n, y[t]);
+#endif
     });
     __syncthreads();  // X is rewritten by the next tile's S1
   }
@@ -254,19 +268,11 @@ template <int N, bool E, bool STAGE, class Prm>
 static cudaError_t launch_t(const Prm& prm, int64_t n_el, cudaStream_t s) {
   using C = Cfg<kBP1, N>;
   constexpr int smem = smem_doubles<kBP1, N>() * int(sizeof(double));
-  static int blocks_per_sm = -1;
-  if (blocks_per_sm < 0) {
-    cudaError_t err = cudaFuncSetAttribute(bp1_kernel<N, E, STAGE>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (err != cudaSuccess) return err;
-    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, bp1_kernel<N, E, STAGE>,
-                                                        C::NT, smem);
-    if (err != cudaSuccess) return err;
-    if (blocks_per_sm < 1) blocks_per_sm = 1;
-  }
   const int64_t ntiles = (n_el + C::EPB - 1) / C::EPB;
-  const int64_t grid = min64(ntiles, int64_t(blocks_per_sm) * sm_count());
-  bp1_kernel<N, E, STAGE><<<unsigned(grid), C::NT, smem, s>>>(prm);
+  unsigned grid = 0;
+  const cudaError_t err = persistent_grid<bp1_kernel<N, E, STAGE>>(C::NT, smem, ntiles, &grid);
+  if (err != cudaSuccess) return err;
+  bp1_kernel<N, E, STAGE><<<grid, C::NT, smem, s>>>(prm);
   return cudaGetLastError();
 }
 

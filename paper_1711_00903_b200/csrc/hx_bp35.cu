@@ -204,19 +204,11 @@ template <int N, bool E, class Prm>
 static cudaError_t launch_t(const Prm& prm, int64_t n_el, cudaStream_t s) {
   using C = Cfg<kBP35, N>;
   constexpr int smem = smem_doubles<kBP35, N>() * int(sizeof(double));
-  static int blocks_per_sm = -1;
-  if (blocks_per_sm < 0) {
-    cudaError_t err = cudaFuncSetAttribute(bp35_kernel<N, E>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (err != cudaSuccess) return err;
-    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, bp35_kernel<N, E>, C::NT,
-                                                        smem);
-    if (err != cudaSuccess) return err;
-    if (blocks_per_sm < 1) blocks_per_sm = 1;
-  }
   const int64_t ntiles = (n_el + C::EPB - 1) / C::EPB;
-  const int64_t grid = min64(ntiles, int64_t(blocks_per_sm) * sm_count());
-  bp35_kernel<N, E><<<unsigned(grid), C::NT, smem, s>>>(prm);
+  unsigned grid = 0;
+  const cudaError_t err = persistent_grid<bp35_kernel<N, E>>(C::NT, smem, ntiles, &grid);
+  if (err != cudaSuccess) return err;
+  bp35_kernel<N, E><<<grid, C::NT, smem, s>>>(prm);
   return cudaGetLastError();
 }
 

@@ -13,14 +13,18 @@
 
 namespace hx {
 
+// SM count of the current device (cached per device ordinal)
 int sm_count() {
-  static int count = 0;
-  if (count == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&count, cudaDevAttrMultiProcessorCount, dev);
-    if (count <= 0) count = 1;
-  }
+  static std::atomic<int> cache[kMaxDevices];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 1;
+  const bool cached = dev >= 0 && dev < kMaxDevices;
+  int count = cached ? cache[dev].load(std::memory_order_relaxed) : 0;
+  if (count > 0) return count;
+  if (cudaDeviceGetAttribute(&count, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+      count <= 0)
+    count = 1;
+  if (cached) cache[dev].store(count, std::memory_order_relaxed);
   return count;
 }
 
@@ -44,8 +48,8 @@ static int kernel_shape(int bp, int degree, int* epb, int* nt, int* smem) {
   return HX_EINVAL;
 }
 
-static cudaError_t launch(const hx_plan& P, const double* q, const double* fac, double* out,
-                          int64_t n_el, int* flag, cudaStream_t s, double* energy = nullptr) {
+cudaError_t launch_apply(const hx_plan& P, const double* q, const double* fac, double* out,
+                         int64_t n_el, int* flag, cudaStream_t s, double* energy) {
   if (n_el == 0) return cudaSuccess;
   switch (P.bp) {
     case HX_BP1:
@@ -76,7 +80,7 @@ static bool centro_ok(const double* M, int R, int C, double sign) {
 
 static thread_local char g_last_cuda[256];
 
-static int cuda_status(cudaError_t err) {
+int cuda_status(cudaError_t err) {
   if (err == cudaSuccess) return HX_OK;
   std::snprintf(g_last_cuda, sizeof(g_last_cuda), "CUDA error: %s",
                 cudaGetErrorString(err));
@@ -128,10 +132,15 @@ int hx_plan_create(int bp, int degree, double lam, const double* interp, const d
 void hx_plan_destroy(hx_plan* P) {
   if (!P) return;
   if (P->pipe_ready) {
+    int cur = 0;
+    const bool moved = cudaGetDevice(&cur) == cudaSuccess && cur != P->pipe_dev;
+    if (moved) cudaSetDevice(P->pipe_dev);
     for (int i = 0; i < 3; ++i) {
       cudaStreamDestroy(P->pipe[i]);
       for (int j = 0; j < hx_host_slots; ++j) cudaEventDestroy(P->ev[i][j]);
     }
+    cudaEventDestroy(P->pipe_last);
+    if (moved) cudaSetDevice(cur);
   }
   delete P;
 }
@@ -174,7 +183,7 @@ int hx_apply(const hx_plan* P, const double* q, const double* factors, double* o
   if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(factors) |
        reinterpret_cast<uintptr_t>(out)) & 7)
     return HX_EINVAL;
-  return cuda_status(launch(*P, q, factors, out, n_el, flag, static_cast<cudaStream_t>(stream)));
+  return cuda_status(launch_apply(*P, q, factors, out, n_el, flag, static_cast<cudaStream_t>(stream)));
 }
 
 int hx_apply_range(const hx_plan* P, const double* q, const double* factors, double* out,
@@ -210,9 +219,18 @@ int hx_interp_elements(int degree, const double* interp, int project, const doub
   if (n_el == 0) return HX_OK;
   if (!src || !dst) return HX_EINVAL;
   if ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 7) return HX_EINVAL;
-  if (!centro_ok(interp, degree + 2, degree + 1, 1.0)) return HX_EINVAL;
-  return cuda_status(launch_interp(degree, interp, project, src, dst, n_el, flag,
-                                   static_cast<cudaStream_t>(stream)));
+  for (int a = 0; a < (degree + 2) * (degree + 1); ++a)
+    if (!std::isfinite(interp[a])) return HX_EINVAL;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (centro_ok(interp, degree + 2, degree + 1, 1.0))
+    return cuda_status(launch_interp(degree, interp, project, src, dst, n_el, flag, s));
+  // any other (N+2) x (N+1) matrix: the dense passes (the reference's
+  // contract_dim accepts every 2-D matrix)
+  const int nsrc = project ? degree + 2 : degree + 1;
+  cudaError_t err = flag ? launch_check_finite(src, n_el * nsrc * nsrc * nsrc, flag, s)
+                         : cudaSuccess;
+  if (err == cudaSuccess) err = launch_interp_dense(degree, interp, project, src, dst, n_el, s);
+  return cuda_status(err);
 }
 
 int64_t hx_apply_host_workspace(const hx_plan* P, int64_t chunk_el) {
@@ -221,12 +239,16 @@ int64_t hx_apply_host_workspace(const hx_plan* P, int64_t chunk_el) {
   return hx_host_slots * 2 /*q,out*/ * chunk_el * n3 * int64_t(sizeof(double));
 }
 
+}  // extern "C"
+
+namespace hx {
+
 // Chunk sizes of the host pipeline: ramp up from chunk_el/8 by doubling,
 // full chunks in the middle, ramp down at the end.  The pipeline's fill (the
 // first H2D runs alone) and drain (the last D2H runs alone) then cost a small
 // chunk each instead of a full one.  Falls back to uniform chunks when the
 // problem is too small for the ramps.
-static std::vector<int64_t> chunk_schedule(int64_t n_el, int64_t chunk_el) {
+std::vector<int64_t> chunk_schedule(int64_t n_el, int64_t chunk_el) {
   std::vector<int64_t> head;
   int64_t ramp = 0;
   for (int64_t c = std::max<int64_t>(1, chunk_el / 8); c < chunk_el; c *= 2) {
@@ -246,6 +268,43 @@ static std::vector<int64_t> chunk_schedule(int64_t n_el, int64_t chunk_el) {
   return out;
 }
 
+// (Re)create the host pipeline's streams and events on the current device.
+cudaError_t pipe_setup(hx_plan* P) {
+  int dev = 0;
+  cudaError_t err = cudaGetDevice(&dev);
+  if (err != cudaSuccess) return err;
+  if (P->pipe_ready && P->pipe_dev == dev) return cudaSuccess;
+  if (P->pipe_ready) {  // the caller moved to another device: rebuild there
+    int cur = dev;
+    cudaSetDevice(P->pipe_dev);
+    for (int i = 0; i < 3; ++i) {
+      cudaStreamSynchronize(P->pipe[i]);
+      cudaStreamDestroy(P->pipe[i]);
+      for (int j = 0; j < hx_host_slots; ++j) cudaEventDestroy(P->ev[i][j]);
+    }
+    cudaEventDestroy(P->pipe_last);
+    cudaSetDevice(cur);
+    P->pipe_ready = false;
+  }
+  for (int i = 0; i < 3; ++i) {
+    if ((err = cudaStreamCreateWithFlags(&P->pipe[i], cudaStreamNonBlocking)) != cudaSuccess)
+      return err;
+    for (int j = 0; j < hx_host_slots; ++j)
+      if ((err = cudaEventCreateWithFlags(&P->ev[i][j], cudaEventDisableTiming)) != cudaSuccess)
+        return err;
+  }
+  if ((err = cudaEventCreateWithFlags(&P->pipe_last, cudaEventDisableTiming)) != cudaSuccess)
+    return err;
+  // nothing recorded yet: waiting on it is a no-op
+  P->pipe_dev = dev;
+  P->pipe_ready = true;
+  return cudaSuccess;
+}
+
+}  // namespace hx
+
+extern "C" {
+
 int hx_apply_host(const hx_plan* Pc, const double* q_host, const double* factors,
                   double* out_host, int64_t n_el, int64_t chunk_el, void* work, int* flag,
                   void* stream) {
@@ -255,18 +314,8 @@ int hx_apply_host(const hx_plan* Pc, const double* q_host, const double* factors
   hx_plan* P = const_cast<hx_plan*>(Pc);  // lazily owned pipeline resources
   std::lock_guard<std::mutex> lock(P->pipe_mu);
   cudaStream_t caller = static_cast<cudaStream_t>(stream);
-  cudaError_t err;
-  if (!P->pipe_ready) {
-    for (int i = 0; i < 3; ++i) {
-      if ((err = cudaStreamCreateWithFlags(&P->pipe[i], cudaStreamNonBlocking)) != cudaSuccess)
-        return cuda_status(err);
-      for (int j = 0; j < hx_host_slots; ++j)
-        if ((err = cudaEventCreateWithFlags(&P->ev[i][j], cudaEventDisableTiming)) !=
-            cudaSuccess)
-          return cuda_status(err);
-    }
-    P->pipe_ready = true;
-  }
+  cudaError_t err = pipe_setup(P);
+  if (err != cudaSuccess) return cuda_status(err);
   const int64_t n3 = int64_t(P->n) * P->n * P->n;
   constexpr int S = hx_host_slots;
   double* wq[S];
@@ -280,43 +329,41 @@ int hx_apply_host(const hx_plan* Pc, const double* q_host, const double* factors
   cudaEvent_t* e_in = P->ev[0];
   cudaEvent_t* e_k = P->ev[1];
   cudaEvent_t* e_out = P->ev[2];
-  // start after whatever the caller queued (e.g. factor generation)
+  // Stream-ordered like every other entry point: all three pipeline streams
+  // start after what the caller queued before this call -- the work that
+  // produces q_host (e.g. an earlier call's D2H into it), earlier users of
+  // `work`, factor generation.
   cudaEvent_t start;
   if ((err = cudaEventCreateWithFlags(&start, cudaEventDisableTiming)) != cudaSuccess)
     return cuda_status(err);
   cudaEventRecord(start, caller);
-  // H2D copies read host memory into our slots: they need only the slot
-  // events -- unless the workspace layout changed since the last call, then
-  // they start after the caller's queue like the kernels and D2H copies
-  const bool cont = P->pipe_work == work && P->pipe_chunk == chunk_el;
-  if (!cont) {
-    cudaStreamWaitEvent(s_in, start, 0);
-    // a previous call's pipeline may still be draining into the same
-    // workspace under another slot layout (or the caller switched streams)
-    if (P->pipe_seq > 0) cudaStreamWaitEvent(s_in, e_out[(P->pipe_seq - 1) % S], 0);
-    P->pipe_seq = 0;
-  }
+  cudaStreamWaitEvent(s_in, start, 0);
   cudaStreamWaitEvent(s_k, start, 0);
   cudaStreamWaitEvent(s_out, start, 0);
+  cudaEventDestroy(start);  // released once recorded work completes
+  // ... and after the plan's previous host-pipeline call, whatever stream it
+  // came from: the pipeline streams and their slot events are shared
+  cudaStreamWaitEvent(s_in, P->pipe_last, 0);
+  cudaStreamWaitEvent(s_k, P->pipe_last, 0);
   const std::vector<int64_t> sched = chunk_schedule(n_el, chunk_el);
   const int64_t nchunks = int64_t(sched.size());
   int64_t e0 = 0;
-  const int64_t seq0 = P->pipe_seq;
   for (int64_t c = 0; c < nchunks; ++c) {
-    const int64_t g = seq0 + c;  // slot sequence number across calls
-    const int slot = int(g % S);
+    const int slot = int(c % S);
     const int64_t ne = sched[c];
     const size_t bytes = size_t(ne * n3) * sizeof(double);
-    if (g >= S) cudaStreamWaitEvent(s_in, e_k[slot], 0);  // kernel g-S done reading wq[slot]
+    if (c >= S) cudaStreamWaitEvent(s_in, e_k[slot], 0);  // kernel c-S done reading wq[slot]
     cudaMemcpyAsync(wq[slot], q_host + e0 * n3, bytes, cudaMemcpyHostToDevice, s_in);
     cudaEventRecord(e_in[slot], s_in);
     cudaStreamWaitEvent(s_k, e_in[slot], 0);
-    if (g >= S) cudaStreamWaitEvent(s_k, e_out[slot], 0);  // D2H g-S done with wo[slot]
-    if ((err = launch(*P, wq[slot], factors + e0 * P->elem_stride, wo[slot], ne, flag, s_k)) !=
+    if (c >= S) cudaStreamWaitEvent(s_k, e_out[slot], 0);  // D2H c-S done with wo[slot]
+    if ((err = launch_apply(*P, wq[slot], factors + e0 * P->elem_stride, wo[slot], ne, flag, s_k)) !=
         cudaSuccess) {
-      cudaEventDestroy(start);
-      P->pipe_work = nullptr;  // the next call starts a fresh slot sequence
-      P->pipe_seq = g;         // ... after the chunks already queued
+      // copies into / out of the caller's host buffers may still be in
+      // flight: finish them before handing the buffers back
+      cudaStreamSynchronize(s_in);
+      cudaStreamSynchronize(s_k);
+      cudaStreamSynchronize(s_out);
       return cuda_status(err);
     }
     cudaEventRecord(e_k[slot], s_k);
@@ -325,12 +372,10 @@ int hx_apply_host(const hx_plan* Pc, const double* q_host, const double* factors
     cudaEventRecord(e_out[slot], s_out);
     e0 += ne;
   }
-  // D2H is in order on one stream: its last chunk done means all are
-  cudaStreamWaitEvent(caller, e_out[(seq0 + nchunks - 1) % S], 0);
-  P->pipe_seq = seq0 + nchunks;
-  P->pipe_work = work;
-  P->pipe_chunk = chunk_el;
-  cudaEventDestroy(start);
+  // D2H is in order on one stream, and it runs after every H2D and kernel
+  // of the call: its last chunk done means the whole pipeline is
+  cudaEventRecord(P->pipe_last, s_out);
+  cudaStreamWaitEvent(caller, P->pipe_last, 0);
   return cuda_status(cudaGetLastError());
 }
 
@@ -344,7 +389,7 @@ int hx_apply_energy(const hx_plan* P, const double* q, const double* factors, do
   if (n_partials < hx_energy_partials()) return HX_EINVAL;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   cudaError_t err = cudaMemsetAsync(partials, 0, sizeof(double) * n_partials, s);
-  if (err == cudaSuccess) err = launch(*P, q, factors, out, n_el, flag, s, partials);
+  if (err == cudaSuccess) err = launch_apply(*P, q, factors, out, n_el, flag, s, partials);
   if (err == cudaSuccess) err = launch_sum(partials, int(n_partials), energy, s);
   return cuda_status(err);
 }

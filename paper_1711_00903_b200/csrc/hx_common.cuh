@@ -13,6 +13,7 @@
 #pragma once
 
 #include <algorithm>
+#include <atomic>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -168,6 +169,51 @@ __device__ __forceinline__ uint64_t l2_evict_first_policy() {
 }
 
 __host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
+
+int sm_count();
+
+// Per-device one-time launch setup of kernel `K`: the dynamic shared-memory
+// opt-in (a function attribute, which lives in each device's context) and
+// the resident-CTA count the persistent grids are sized by.  Cached per
+// (kernel, device ordinal), so one process can drive several GPUs; the
+// setup is idempotent, so two threads racing on a first launch are harmless.
+constexpr int kMaxDevices = 64;
+
+template <auto K>
+inline cudaError_t resident_blocks(int threads, int smem, int* blocks) {
+  static std::atomic<int> cache[kMaxDevices];  // 0: not set up on that device yet
+  int dev = 0;
+  cudaError_t err = cudaGetDevice(&dev);
+  if (err != cudaSuccess) return err;
+  if (dev >= 0 && dev < kMaxDevices) {
+    const int c = cache[dev].load(std::memory_order_relaxed);
+    if (c > 0) {
+      *blocks = c;
+      return cudaSuccess;
+    }
+  }
+  if (smem > 48 * 1024) {
+    err = cudaFuncSetAttribute(K, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (err != cudaSuccess) return err;
+  }
+  int b = 0;
+  err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, K, threads, smem);
+  if (err != cudaSuccess) return err;
+  if (b < 1) b = 1;
+  if (dev >= 0 && dev < kMaxDevices) cache[dev].store(b, std::memory_order_relaxed);
+  *blocks = b;
+  return cudaSuccess;
+}
+
+// Persistent grid for `ntiles` tiles of kernel K on the current device.
+template <auto K>
+inline cudaError_t persistent_grid(int threads, int smem, int64_t ntiles, unsigned* grid) {
+  int b = 0;
+  cudaError_t err = resident_blocks<K>(threads, smem, &b);
+  if (err != cudaSuccess) return err;
+  *grid = unsigned(min64(ntiles, int64_t(b) * sm_count()));
+  return cudaSuccess;
+}
 
 __device__ __forceinline__ bool nonfinite(double v) {
   // exponent all ones <=> inf or nan

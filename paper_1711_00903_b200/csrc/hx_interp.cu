@@ -153,19 +153,11 @@ template <int N, bool PROJECT>
 static cudaError_t launch_interp_t(const InterpParams<N>& prm, cudaStream_t s) {
   using C = Cfg<kBP1, N>;
   constexpr int smem = (C::EBUF[0] + C::EBUF[1]) * C::EPB * int(sizeof(double));
-  static int blocks_per_sm = -1;
-  if (blocks_per_sm < 0) {
-    cudaError_t err = cudaFuncSetAttribute(interp_kernel<N, PROJECT>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (err != cudaSuccess) return err;
-    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, interp_kernel<N, PROJECT>,
-                                                        C::NT, smem);
-    if (err != cudaSuccess) return err;
-    if (blocks_per_sm < 1) blocks_per_sm = 1;
-  }
   const int64_t ntiles = (prm.n_el + C::EPB - 1) / C::EPB;
-  const int64_t grid = min64(ntiles, int64_t(blocks_per_sm) * sm_count());
-  interp_kernel<N, PROJECT><<<unsigned(grid), C::NT, smem, s>>>(prm);
+  unsigned grid = 0;
+  const cudaError_t err = persistent_grid<interp_kernel<N, PROJECT>>(C::NT, smem, ntiles, &grid);
+  if (err != cudaSuccess) return err;
+  interp_kernel<N, PROJECT><<<grid, C::NT, smem, s>>>(prm);
   return cudaGetLastError();
 }
 

@@ -3,6 +3,7 @@
 
 #include <cstdint>
 #include <mutex>
+#include <vector>
 #include <cuda_runtime.h>
 
 #include "../../include/hexbench_b200.h"
@@ -30,23 +31,27 @@ struct hx_plan {
   int n_slots;            // factor slots kept on device (1 for BP1, 7 otherwise)
   int64_t slot_stride;    // doubles per slot (q^3 rounded up to even)
   int64_t elem_stride;    // doubles per element (n_slots * slot_stride)
-  // lazily created resources for the host-buffer (end-to-end) path; `pipe_mu`
-  // serialises hx_apply_host calls on one plan (they share these streams and
-  // events), everything else about a plan is immutable after create
+  // lazily created resources for the host-buffer (end-to-end) path, on
+  // device `pipe_dev`; `pipe_mu` serialises hx_apply_host calls on one plan
+  // (they share these streams and events), everything else about a plan is
+  // immutable after create
   cudaStream_t pipe[3];
   cudaEvent_t ev[3][hx_host_slots];
+  cudaEvent_t pipe_last;  // end of the plan's latest host-pipeline call
   bool pipe_ready;
+  int pipe_dev = -1;
   std::mutex pipe_mu;
-  // chunk slots persist across hx_apply_host calls: a call that reuses the
-  // previous call's workspace and chunk size continues the slot sequence, so
-  // its H2D copies only wait for the slots they reuse (not for the whole
-  // previous call) and back-to-back calls overlap their transfers
-  int64_t pipe_seq = 0;
-  const void* pipe_work = nullptr;
-  int64_t pipe_chunk = 0;
 };
 
 namespace hx {
+
+// the fused kernel of the plan's operator (energy: per-CTA <q, A q> partials)
+cudaError_t launch_apply(const hx_plan& P, const double* q, const double* fac, double* out,
+                         int64_t n_el, int* flag, cudaStream_t s, double* energy = nullptr);
+// host pipeline helpers (hx_capi.cu): chunk sizes, lazily built streams
+std::vector<int64_t> chunk_schedule(int64_t n_el, int64_t chunk_el);
+cudaError_t pipe_setup(hx_plan* P);
+int cuda_status(cudaError_t err);
 
 // launch the fused element kernel for elements [0, n_el) of device arrays
 cudaError_t launch_bp1(const hx_plan& P, const double* q, const double* fac, double* out,
@@ -60,6 +65,9 @@ cudaError_t launch_baseline(const hx_plan& P, const double* q, const double* fac
 int64_t baseline_workspace_doubles(const hx_plan& P, int64_t n_el);
 cudaError_t launch_interp(int degree, const double* interp, int project, const double* src,
                           double* dst, int64_t n_el, int* flag, cudaStream_t s);
+cudaError_t launch_interp_dense(int degree, const double* interp, int project, const double* src,
+                                double* dst, int64_t n_el, cudaStream_t s);
+cudaError_t launch_check_finite(const double* x, int64_t n, int* flag, cudaStream_t s);
 cudaError_t launch_geometry(const hx_plan& P, const double* verts, int64_t n_el, int all_slots,
                             double* fac, int* flag, cudaStream_t s);
 cudaError_t launch_repack(const hx_plan& P, const double* src, int64_t n_el, double* dst,

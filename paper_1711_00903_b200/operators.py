@@ -241,6 +241,10 @@ def apply_device(op, q, out, flag=None, stream=None):
     """Raw device apply: ``out = A q`` for torch CUDA tensors, asynchronous on
     ``stream`` (default: torch's current stream), no allocation, no sync.
     This is what the harness times."""
+    import torch
+    if torch.cuda.current_device() != op.device.index:
+        with torch.cuda.device(op.device):
+            return apply_device(op, q, out, flag, stream)
     if stream is None:
         stream = _stream(op.device)
     _native.check(_native.lib().hx_apply(
@@ -248,111 +252,147 @@ def apply_device(op, q, out, flag=None, stream=None):
         op.n_el, _native.ptr(flag), stream), "hx_apply")
 
 
+def _check_out(op, q, out):
+    """A caller-supplied ``out`` must be what the kernels write without a
+    copy: C-contiguous float64 of shape (n_el, n_p), the same kind as ``q``
+    (a CUDA tensor on op.device for device data, host memory for host data),
+    and not ``q`` itself."""
+    shape = (op.n_el, op.n_p)
+    if q.on_device:
+        import torch
+        if not (_is_torch(out) and out.is_cuda):
+            raise ValueError("out must be a CUDA tensor when q is device-resident")
+        if out.device != op.device:
+            raise ValueError(f"out is on {out.device}, the operator on {op.device}")
+        if out.dtype != torch.float64 or tuple(out.shape) != shape or not out.is_contiguous():
+            raise ValueError(f"out must be a contiguous float64 tensor of shape {shape}")
+        if out.data_ptr() == q.data.data_ptr():
+            raise ValueError("out must not alias q")
+    else:
+        if not isinstance(out, np.ndarray):
+            raise ValueError("out must be a numpy array when q is host data")
+        if out.dtype != np.float64 or out.shape != shape or not out.flags.c_contiguous \
+                or not out.flags.writeable:
+            raise ValueError(f"out must be a writeable C-contiguous float64 array of shape {shape}")
+        if np.shares_memory(out, q.data):
+            raise ValueError("out must not alias q")
+
+
 def apply_operator(op, q, counters=None, threads=1, out=None):
     """Apply a benchmark operator to a field vector (reference operators.py:306-331).
 
     Returns a new FieldVector of the same kind as ``q`` (host numpy in, host
     numpy out; device tensor in, device tensor out).  Raises ValueError on a
-    shape mismatch or non-finite input, like the reference.
+    shape mismatch, a device mismatch or non-finite input, like the
+    reference.  Without ``out`` the non-finite test is fused into the kernel's
+    loads and the (never returned) result is discarded on error; with a
+    caller-supplied ``out`` (an extension: the reference has none) q is
+    scanned first, as the reference does (operators.py:317-318), so ``out``
+    is left untouched on bad input.
     """
     if q.n_el != op.n_el or q.n_p != op.n_p:
         raise ValueError("field vector shape does not match operator")
     import torch
 
     dev = op.device
+    if q.on_device and q.data.device != dev:
+        raise ValueError(f"field vector is on {q.data.device}, the operator on {dev}")
+    if out is not None:
+        _check_out(op, q, out)
     with torch.cuda.device(dev):
         flag = torch.zeros(1, dtype=torch.int32, device=dev)
         stream = _stream(dev)
         if q.on_device:
             src = q.data.contiguous()
+            if out is not None:
+                _native.check(_native.lib().hx_check_finite(
+                    _native.ptr(src), src.numel(), _native.ptr(flag), stream), "hx_check_finite")
+                if int(flag.item()) & _native.HX_FLAG_NONFINITE:
+                    raise ValueError("field vector contains non-finite values")
             dst = torch.empty_like(src) if out is None else out
             apply_device(op, src, dst, flag, stream)
             result = FieldVector(op.n_el, op.n_p, dst)
         else:
             src = np.ascontiguousarray(q.data, dtype=np.float64)
-            dst = np.empty_like(src) if out is None else out
-            result = FieldVector(op.n_el, op.n_p, _apply_numpy(op, src, dst, flag, stream))
+            if out is not None and not _native.lib().hx_host_all_finite(
+                    _native.ptr(src), src.size):
+                raise ValueError("field vector contains non-finite values")
+            dst = _pinned_empty(src.shape) if out is None else out
+            _apply_numpy(op, src, dst, flag, stream)
+            result = FieldVector(op.n_el, op.n_p, dst)
         if int(flag.item()) & _native.HX_FLAG_NONFINITE:
             raise ValueError("field vector contains non-finite values")
     _charge(op, counters)
     return result
 
 
-DEFAULT_CHUNK_BYTES = 32 << 20  # r42: best with the cross-call slot pipeline
+DEFAULT_CHUNK_BYTES = 32 << 20  # r42: best for isolated pinned calls
+STAGED_CHUNK_BYTES = 16 << 20   # pageable input: host copy of chunk c+1 overlaps chunk c
 
 
 def host_chunk_elements(op, chunk_bytes=DEFAULT_CHUNK_BYTES):
     return max(1, min(op.n_el, chunk_bytes // (op.n_p * DOUBLE)))
 
 
-def _apply_host(op, src, dst, flag, stream, chunk_el=None, work=None):
+def _device_work(op, chunk_el):
     import torch
+    nbytes = _native.lib().hx_apply_host_workspace(op.plan.handle, chunk_el)
+    return torch.empty(nbytes // DOUBLE, dtype=torch.float64, device=op.device)
+
+
+def _apply_host(op, src, dst, flag, stream, chunk_el=None, work=None):
     if op.n_el == 0:
         return dst
     if chunk_el is None:
         chunk_el = host_chunk_elements(op)
     if work is None:
-        nbytes = _native.lib().hx_apply_host_workspace(op.plan.handle, chunk_el)
-        work = torch.empty(nbytes // DOUBLE, dtype=torch.float64, device=op.device)
+        work = _device_work(op, chunk_el)
     _native.check(_native.lib().hx_apply_host(
         op.plan.handle, _native.ptr(src), _native.ptr(op.device_factors), _native.ptr(dst),
         op.n_el, chunk_el, _native.ptr(work), _native.ptr(flag), stream), "hx_apply_host")
     return dst
 
 
-# Pageable numpy arrays: DMA from pageable memory is staged by the driver one
-# synchronous bounce at a time (~6 GB/s here; page-locking 134 MB per call
-# costs ~190 ms).  Large arrays are instead copied with host threads into a
-# cached page-locked staging pair and sent through the pinned pipeline
-# (tools/host_paths.py: BP3.5 E=32768 42 ms pageable vs ~3 ms pinned).
-_STAGING_MIN_BYTES = 8 << 20
+def _pinned_empty(shape):
+    """Uninitialised page-locked float64 host array (torch's caching host
+    allocator: repeated calls reuse the blocks), so apply_operator's result
+    comes straight back over PCIe with no host copy or page faults."""
+    import torch
+    return torch.empty(int(np.prod(shape)), dtype=torch.float64,
+                       pin_memory=True).numpy().reshape(shape)
+
+
+# Page-locked staging ring of hx_apply_host_staged, cached per size; one user
+# at a time.
 _staging = {}
-_copy_pool = None
-_staging_lock = threading.Lock()  # one staging pair, one user at a time
+_staging_lock = threading.Lock()
 
 
-def _parallel_copy(dst, src):
-    """dst[:] = src with the host's cores (numpy releases the GIL)."""
-    global _copy_pool
-    import os
-    from concurrent.futures import ThreadPoolExecutor
-
-    n = src.shape[0]
-    workers = max(1, min(16, os.cpu_count() or 1))
-    if _copy_pool is None:
-        _copy_pool = ThreadPoolExecutor(max_workers=workers)
-    bounds = np.linspace(0, n, workers + 1).astype(int)
-    list(_copy_pool.map(lambda lh: np.copyto(dst[lh[0]:lh[1]], src[lh[0]:lh[1]]),
-                        [(lo, hi) for lo, hi in zip(bounds[:-1], bounds[1:]) if hi > lo]))
-
-
-def _pinned_pair(shape):
-    """Cached page-locked (q, out) staging arrays of at least `shape`."""
+def _staging_buffer(op, chunk_el):
     import torch
-
-    need = int(np.prod(shape))
-    have = _staging.get("n", 0)
-    if have < need:
-        _staging["q"] = torch.empty(need, dtype=torch.float64).pin_memory()
-        _staging["out"] = torch.empty(need, dtype=torch.float64).pin_memory()
-        _staging["n"] = need
-    return (_staging["q"][:need].numpy().reshape(shape),
-            _staging["out"][:need].numpy().reshape(shape))
+    need = _native.lib().hx_apply_host_staging_bytes(op.plan.handle, chunk_el) // DOUBLE
+    buf = _staging.get("buf")
+    if buf is None or buf.numel() < need:
+        buf = torch.empty(need, dtype=torch.float64, pin_memory=True)
+        _staging["buf"] = buf
+    return buf
 
 
-def _apply_numpy(op, src, dst, flag, stream):
-    """apply_operator's host path: pinned pipeline through a staging pair for
-    large pageable arrays, the direct pipeline otherwise."""
-    import torch
-
-    if src.nbytes < _STAGING_MIN_BYTES:
-        return _apply_host(op, src, dst, flag, stream)
+def _apply_numpy(op, src, dst, flag, stream, chunk_el=None):
+    """apply_operator's host path: hx_apply_host_staged, which streams
+    pageable arrays through a pinned ring with host worker threads (page-
+    locked ones go straight to the copy engines).  Host-synchronous."""
+    if op.n_el == 0:
+        return dst
+    if chunk_el is None:
+        chunk_el = host_chunk_elements(op, STAGED_CHUNK_BYTES)
+    work = _device_work(op, chunk_el)
     with _staging_lock:
-        qs, os_ = _pinned_pair(src.shape)
-        _parallel_copy(qs, src)
-        _apply_host(op, qs, os_, flag, stream)
-        torch.cuda.current_stream(op.device).synchronize()
-        _parallel_copy(dst, os_)
+        stage = _staging_buffer(op, chunk_el)
+        _native.check(_native.lib().hx_apply_host_staged(
+            op.plan.handle, _native.ptr(src), _native.ptr(op.device_factors),
+            _native.ptr(dst), op.n_el, chunk_el, _native.ptr(work), _native.ptr(stage),
+            _native.ptr(flag), stream), "hx_apply_host_staged")
     return dst
 
 

@@ -1,6 +1,7 @@
 """CPU: the drop-in API surface and its validation (reference
 tests/test_operators.py:245-264 and operators.py:120-129, 315-318, 334-349)."""
 
+import pathlib
 import numpy as np
 import pytest
 
@@ -198,3 +199,33 @@ def test_report_calibrate_usage_errors():
     from paper_1711_00903_b200.report import main
     assert main(["calibrate", "--bytes", "100"]) == 2
     assert main(["calibrate", "--bytes", str(1 << 22), "--repeats", "2"]) == 2
+
+
+def _bench(*args, env=None):
+    import json
+    import subprocess
+    import sys
+    root = pathlib.Path(__file__).resolve().parent.parent
+    res = subprocess.run([sys.executable, str(root / "bench.py"), *args], capture_output=True,
+                         text=True, timeout=600, cwd=root, env=env)
+    assert res.returncode == 0, res.stderr[-3000:]
+    lines = [line for line in res.stdout.splitlines() if line.startswith("{")]
+    assert len(lines) == 1, res.stdout[-2000:]
+    return json.loads(lines[0])
+
+
+def test_reference_arm_runs_the_reference_on_cpu():
+    """bench.py --impl reference needs no GPU: it times the unmodified
+    reference (baseline/_ref, tools/install_reference.sh) on the host."""
+    d = _bench("--impl", "reference", "--steps", "1", "--warmup", "3")
+    assert d["impl"] == "reference" and d["value"] > 0 and d["n_gpus"] == 1
+    assert d["cpu_baseline"]["kind"] in ("reference", "port")
+    assert d["cpu_baseline"]["value"] == d["value"]
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
+
+
+def test_reference_arm_gpus_2_relaunch_prints_one_line():
+    """--gpus 2 outside torchrun re-launches under torch.distributed.run;
+    only rank 0 runs the reference arm and prints."""
+    d = _bench("--impl", "reference", "--gpus", "2", "--steps", "1", "--warmup", "3")
+    assert d["impl"] == "reference" and d["n_gpus"] == 2

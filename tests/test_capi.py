@@ -123,3 +123,17 @@ def test_missing_library_fails_loudly(monkeypatch, tmp_path):
     monkeypatch.setattr(_native, "_lib", None)
     with pytest.raises(_native.NativeLibraryError):
         _native.lib()
+
+
+def test_host_finite_scan_runs_on_host_threads():
+    """hx_host_all_finite (the up-front np.isfinite scan of operators.py:317,
+    for apply_operator(..., out=)) is host-only: no GPU needed."""
+    x = np.random.default_rng(0).standard_normal(3_000_001)
+    lib = _native.lib()
+    assert lib.hx_host_all_finite(x.ctypes.data, x.size) == 1
+    assert lib.hx_host_all_finite(x.ctypes.data, 0) == 1
+    for pos in (0, 1_500_000, 3_000_000):
+        for v in (np.inf, -np.inf, np.nan):
+            y = x.copy()
+            y[pos] = v
+            assert lib.hx_host_all_finite(y.ctypes.data, y.size) == 0

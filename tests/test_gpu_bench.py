@@ -45,14 +45,45 @@ def test_bench_line_contract():
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert d["cpu_baseline"]["kind"] in ("port", "reference") and d["cpu_baseline"]["cores"] >= 1
     assert d["gpu_launches"] >= 3
-    for leg in ("per_bp", "cg", "cg_assembled", "unfused_baseline", "calibration"):
-        assert d.get(leg), leg
+    assert d["cpu_baseline"]["kind"] == "reference"  # baseline/_ref travels with the repo
+    assert d["e2e"]["api"]["value"] > 0
+    # per_bp is the line's LAST key (the driver keeps the tail) and slim
+    assert list(d)[-1] == "per_bp"
+    assert set(d["per_bp"]) == {"BP3.5 E=32768", "BP1.0 E=4096", "BP3.0 E=32768",
+                                "BP1.0 E=32768"}
+    for rep in d["per_bp"].values():
+        assert rep["gdof_per_s"] > 0 and 0 < rep["frac_of_measured_peak"] < 1.3
+        assert 0 < rep["smem_roofline_frac"] < 1.0
+    assert len(json.dumps(d["per_bp"])) < 1200
+    with open(os.path.join(ROOT, d["details"]["file"])) as fh:
+        details = json.load(fh)
+    for leg in ("per_bp", "cg", "cg_assembled", "unfused_baseline", "calibration", "e2e_api"):
+        assert details.get(leg), leg
 
 
-def test_reference_arm_contract():
-    d = _run("--impl", "reference", "--steps", "1", "--warmup", "3")
-    assert d["impl"] == "reference" and d["value"] > 0
-    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["value"] == d["value"]
+def test_bench_gpus_2_relaunches_itself():
+    """Plain `python bench.py --gpus 2` (how the driver calls it) runs two
+    ranks: it re-launches itself under torch.distributed.run (here over gloo,
+    sharing the one GPU; NCCL with one GPU per rank on a multi-GPU node)."""
+    env = dict(os.environ, HX_BENCH_BACKEND="gloo")
+    res = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2",
+                          "--quick", "--steps", "3", "--warmup", "3"],
+                         capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    assert res.returncode == 0, res.stderr[-3000:]
+    lines = [line for line in res.stdout.splitlines() if line.startswith("{")]
+    assert len(lines) == 1, res.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and "x2" in d["config"]["parallelism"] and d["value"] > 0
+
+
+def test_bench_refuses_more_nccl_ranks_than_gpus():
+    if torch.cuda.device_count() > 1:
+        pytest.skip("multi-GPU node")
+    res = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2",
+                          "--quick", "--steps", "3"],
+                         capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert res.returncode != 0
+    assert "need 2 GPUs" in res.stderr
 
 
 def test_bench_two_ranks_weak_scaling_line():

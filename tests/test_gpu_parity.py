@@ -310,6 +310,27 @@ def test_full_size_config_sampled_parity_and_symmetry(bp):
     assert float((aw - (2 * au - av)).norm() / aw.norm()) <= 1e-14
 
 
+def test_full_size_device_factors_match_reference_sample():
+    """Device geometric factors of the whole E=32768 BASELINE mesh against
+    the reference's geometric_factors (mesh.py:101-139) on 24 sampled
+    elements (tests/golden/factors_e32768.npz, make_factor_sample.py), for
+    the GLL(8) rule of BP3.5 and the GL(9) rule of BP1.0 / BP3.0."""
+    import os
+    fx = np.load(os.path.join(os.path.dirname(__file__), "golden", "factors_e32768.npz"))
+    idx = fx["elements"]
+    mesh = hx.perturb_mesh(hx.build_cube_mesh(32, 2.0), amplitude=0.15, seed=7)
+    np.testing.assert_array_equal(mesh.vertices[idx], fx["vertices"])
+    for bp, key in ((hx.BP35, "gll8"), (hx.BP3, "gl9"), (hx.BP1, "gl9")):
+        op = hx.make_operator(bp, 7, mesh)
+        q = 8 if bp == hx.BP35 else 9
+        ref = fx[key].reshape(len(idx), 7, q ** 3)
+        packed = op.device_factors.view(mesh.n_el, op.plan.elem_stride)[torch.from_numpy(idx)]
+        got = packed.view(len(idx), op.plan.n_slots, op.plan.slot_stride)[:, :, :q ** 3]
+        got = got.cpu().numpy()
+        want = ref if op.plan.n_slots == 7 else ref[:, 6:7]
+        assert orc.rel_l2(got, want) <= 1e-14, (bp, orc.rel_l2(got, want))
+
+
 @pytest.mark.parametrize("bp", BPS)
 @pytest.mark.parametrize("deg", [1, 2, 4, 7, 8, 15])
 def test_unfused_baseline_path_matches_oracle(bp, deg, mesh3):

@@ -5,8 +5,10 @@
 
 Reads every prof_*.ncu-rep under the run directory and writes
 ``<dest>_ncu.md`` (key metrics + top stall reasons per kernel) and updates
-``profiles/traffic.json`` (DRAM bytes per launch, consumed by bench.py's
-roofline.traffic).
+``profiles/kernels.json``: per kernel (canonical key ``kernel<N>``) the DRAM
+bytes, shared-memory wavefronts and pipe utilisations of one launch over
+``n_el`` elements (the profile_one.py size, 32768 by default; override with
+HX_NCU_N_EL) -- bench.py's roofline.traffic and per_bp smem roofline read it.
 """
 
 import csv
@@ -24,8 +26,11 @@ KEYS = [
     ("dram__bytes_write.sum", "DRAM write"),
     ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "DRAM throughput % of peak"),
     ("lts__t_sector_hit_rate.pct", "L2 hit rate %"),
+    ("l1tex__data_pipe_lsu_wavefronts.sum.pct_of_peak_sustained_elapsed",
+     "L1 LSU data pipe (shared + global wavefronts) % of peak"),
     ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
      "smem wavefronts % of peak"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "smem wavefronts"),
     ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum", "smem ld bank conflicts"),
     ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_st.sum", "smem st bank conflicts"),
     ("l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum", "smem ld wavefronts"),
@@ -60,8 +65,9 @@ def main(run_dir, dest, launches=None):
              "Captured with `ncu --set full --clock-control none --import-source on` "
              "(one launch per kernel, tools/profile_one.py at the BASELINE size). "
              "Absolute times are cold-cache single launches.", ""]
-    tpath = os.path.join(os.path.dirname(dest) or ".", "traffic.json")
-    traffic = json.load(open(tpath)) if os.path.exists(tpath) else {}
+    kpath = os.path.join(os.path.dirname(dest) or ".", "kernels.json")
+    kernels = json.load(open(kpath)) if os.path.exists(kpath) else {}
+    n_el = int(os.environ.get("HX_NCU_N_EL", "32768"))
     for rep in sorted(glob.glob(os.path.join(run_dir, "prof_*.ncu-rep"))):
         for rec in raw(rep):
             name = rec.get("Kernel Name", ("", "?"))[1]
@@ -88,14 +94,33 @@ def main(run_dir, dest, launches=None):
                          ", ".join(f"{n} {v:.2f}" for v, n in stalls[:6]))
             lines.append("")
             if "dram__bytes_read.sum" in rec:
-                rb = to_bytes(*rec["dram__bytes_read.sum"])
-                wb = to_bytes(*rec["dram__bytes_write.sum"])
                 short = name.split("(")[0].replace("void ", "").replace("hx::", "")
                 # canonical key: kernel<N> (the other template flags -- energy,
                 # staging -- do not change the plain apply's traffic)
                 base, _, targs = short.partition("<")
                 key = f"{base}<{targs.split(',')[0].rstrip('>').strip()}>" if targs else short
-                traffic[key] = rb + wb
+
+                def num(k):
+                    return float(rec[k][1].replace(",", "")) if k in rec else None
+                kernels[key] = {
+                    "n_el": n_el,
+                    "source": f"{os.path.basename(dest)}_ncu.md ({os.path.basename(rep)})",
+                    "duration_ns": num("gpu__time_duration.sum") * {
+                        "nsecond": 1, "ns": 1, "usecond": 1e3, "us": 1e3, "msecond": 1e6,
+                        "ms": 1e6}.get(rec["gpu__time_duration.sum"][0], 1),
+                    "dram_bytes": to_bytes(*rec["dram__bytes_read.sum"]) +
+                    to_bytes(*rec["dram__bytes_write.sum"]),
+                    "smem_wavefronts": num("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"),
+                    "smem_ld_wavefronts": num("l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum"),
+                    "smem_st_wavefronts": num("l1tex__data_pipe_lsu_wavefronts_mem_shared_op_st.sum"),
+                    "smem_bank_conflicts": (num("l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum") or 0) +
+                    (num("l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_st.sum") or 0),
+                    "l1_lsu_pipe_pct": num("l1tex__data_pipe_lsu_wavefronts.sum.pct_of_peak_sustained_elapsed"),
+                    "smem_pipe_pct": num("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed"),
+                    "fp64_pipe_pct": num("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+                    "issue_pct": num("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                    "registers": num("launch__registers_per_thread"),
+                }
     if launches and os.path.exists(launches):
         lines.append("## Launch list (`gpu__time_duration.sum`, cold-cache, serialised)")
         lines.append("")
@@ -110,9 +135,9 @@ def main(run_dir, dest, launches=None):
         lines.append("")
     with open(dest + "_ncu.md", "w") as fh:
         fh.write("\n".join(lines) + "\n")
-    with open(tpath, "w") as fh:
-        json.dump(traffic, fh, indent=1, sort_keys=True)
-    print(f"wrote {dest}_ncu.md and {tpath}")
+    with open(kpath, "w") as fh:
+        json.dump(kernels, fh, indent=1, sort_keys=True)
+    print(f"wrote {dest}_ncu.md and {kpath}")
 
 
 if __name__ == "__main__":
