@@ -14,7 +14,9 @@
  *     (reference operators.py:67-79).
  *   - factors: packed device layout, per element `n_slots` slots of
  *     `slot_stride` doubles (see hx_plan_factor_layout).  Slot order is the
- *     reference's FACTOR_NAMES (mesh.py:12); BP1.0 keeps only GwJ.
+ *     reference's FACTOR_NAMES (mesh.py:12); BP1.0 keeps only GwJ, stored
+ *     i-major: point (k, j, i) at i*q^2 + k*q + j (every other slot is in the
+ *     reference point order, k*q^2 + j*q + i).
  *   - every call that takes a `stream` is asynchronous on that cudaStream_t
  *     (NULL = legacy default stream) and never synchronises the device.
  *   - status: 0 on success, otherwise an HX_E* code; hx_strerror explains it.

@@ -26,7 +26,7 @@
 
 namespace hx {
 
-enum { kBP1 = 10, kBP35 = 35, kBP3 = 30 };
+enum { kBP1 = 10, kBP35 = 35, kBP3 = 30, kINTERP = 11 };  // kINTERP: hx_interp.cu shapes
 
 template <int R, int C>
 struct Fold {

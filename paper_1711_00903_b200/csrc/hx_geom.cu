@@ -59,11 +59,12 @@ __global__ void geometry_kernel(const __grid_constant__ GeomParams p) {
   const double det = a[0][0] * adj[0][0] + a[0][1] * adj[1][0] + a[0][2] * adj[2][0];
   if (!(det > 1e-14) && p.flag) atomicOr(p.flag, 2);
   const double w3 = p.weights[ii] * p.weights[jj] * p.weights[kk];
-  double* dst = p.fac + e * p.estride + pt;
   if (p.gwj_only) {
-    dst[0] = w3 * det;
+    // BP1.0's packed slot is i-major (hx_bp1.cu S3): point (k, j, i) at i*q^2 + k*q + j
+    p.fac[e * p.estride + (ii * q + kk) * q + jj] = w3 * det;
     return;
   }
+  double* dst = p.fac + e * p.estride + pt;
   const double sc = w3 / det;
   auto g = [&](int x, int y) {
     return sc * (adj[x][0] * adj[y][0] + adj[x][1] * adj[y][1] + adj[x][2] * adj[y][2]);
@@ -102,8 +103,9 @@ cudaError_t launch_geometry(const hx_plan& P, const double* verts, int64_t n_el,
 
 // Reference layout (E, 7, q^3) <-> packed layout (E, nslot, sstride).
 __global__ void repack_kernel(const double* __restrict__ src, double* __restrict__ dst,
-                              int64_t n_el, int q3, int nslot, int first_slot, int64_t sstride,
-                              int to_packed) {
+                              int64_t n_el, int q, int nslot, int first_slot, int64_t sstride,
+                              int to_packed, int imajor) {
+  const int q3 = q * q * q;
   const int64_t gid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t per = int64_t(nslot) * q3;
   if (gid >= n_el * per) return;
@@ -111,7 +113,13 @@ __global__ void repack_kernel(const double* __restrict__ src, double* __restrict
   const int rem = int(gid % per);
   const int sl = rem / q3, pt = rem % q3;
   const int64_t ref = (e * 7 + first_slot + sl) * q3 + pt;
-  const int64_t pk = (e * nslot + sl) * sstride + pt;
+  // BP1.0's single packed slot is i-major (hx_bp1.cu S3): (k, j, i) at i*q^2 + k*q + j
+  int ppt = pt;
+  if (imajor) {
+    const int kk = pt / (q * q), jj = (pt / q) % q, ii = pt % q;
+    ppt = (ii * q + kk) * q + jj;
+  }
+  const int64_t pk = (e * nslot + sl) * sstride + ppt;
   if (to_packed)
     dst[pk] = src[ref];
   else
@@ -127,8 +135,9 @@ cudaError_t launch_repack(const hx_plan& P, const double* src, int64_t n_el, dou
   const int first = (to_packed && P.n_slots == 1) ? 6 : 0;
   const int64_t total = n_el * int64_t(nslot) * q3;
   const int threads = 256;
+  const int imajor = to_packed && P.n_slots == 1;
   repack_kernel<<<unsigned((total + threads - 1) / threads), threads, 0, s>>>(
-      src, dst, n_el, q3, nslot, first, P.slot_stride, to_packed);
+      src, dst, n_el, P.q, nslot, first, P.slot_stride, to_packed, imajor);
   return cudaGetLastError();
 }
 

@@ -3,10 +3,11 @@
 //   interpolate_to_gl(q_e, I) = I_k ( I_r ( I_s q_e ) )   (n,n,n) -> (m,m,m)
 //   project_to_gll(t_e, I)    = I^T applied along the same three axes
 //
-// batched over elements.  Same building blocks and shared-memory layouts as
-// the BP1.0 kernel (Cfg<kBP1, N>: X is (n,m,n), Y is (n,m,m)); BP1.0 is
+// batched over elements.  Same building blocks as the BP1.0 kernel (BP1.0 is
 // exactly project(GwJ * interpolate(q)), these are its two halves without the
-// pointwise scale.  Stage order:
+// pointwise scale), in the (s, r, t) stage order that ends / starts with
+// coalesced k-lines on the GL side (Cfg<kINTERP, N>: X is (n,m,n), Y is
+// (n,m,m)).  Stage order:
 //
 //   interpolate  S1 j-lines (k,i)  src -> I_s -> X ; S2 i-lines (k,a) X -> I_r -> Y ;
 //                S3 k-lines (a,c)  Y -> I_t -> dst (HBM, coalesced)
@@ -31,9 +32,9 @@ struct InterpParams {
 };
 
 template <int N, bool PROJECT>
-__global__ void __launch_bounds__(Cfg<kBP1, N>::NT)
+__global__ void __launch_bounds__(Cfg<kINTERP, N>::NT)
     interp_kernel(const __grid_constant__ InterpParams<N> p) {
-  using C = Cfg<kBP1, N>;
+  using C = Cfg<kINTERP, N>;
   constexpr int n = N + 1, m = N + 2, n2 = n * n, n3 = n2 * n, m2 = m * m, m3 = m2 * m;
   constexpr int EPB = C::EPB, NT = C::NT;
   constexpr Lay LX = C::L[0], LY = C::L[1];
@@ -151,7 +152,7 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT)
 
 template <int N, bool PROJECT>
 static cudaError_t launch_interp_t(const InterpParams<N>& prm, cudaStream_t s) {
-  using C = Cfg<kBP1, N>;
+  using C = Cfg<kINTERP, N>;
   constexpr int smem = (C::EBUF[0] + C::EBUF[1]) * C::EPB * int(sizeof(double));
   const int64_t ntiles = (prm.n_el + C::EPB - 1) / C::EPB;
   unsigned grid = 0;

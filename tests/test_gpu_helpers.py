@@ -110,7 +110,12 @@ def test_errors():
     with pytest.raises(ValueError):
         hx.interpolate_to_gl(np.full((4, 4, 4), np.nan), mat)  # non-finite
     with pytest.raises(ValueError):
-        hx.interpolate_to_gl(np.zeros((4, 4, 4)), np.ones((5, 4)) + np.eye(5, 4))  # not centro
+        hx.interpolate_to_gl(np.zeros((4, 4, 4)), np.full((5, 4), np.inf))  # non-finite matrix
+    # any other finite matrix is accepted (dense passes), like contract_dim
+    m = np.ones((5, 4)) + np.eye(5, 4)
+    q = np.random.default_rng(0).standard_normal((4, 4, 4))
+    np.testing.assert_allclose(hx.interpolate_to_gl(q, m), orc.interp_passes(m, q[None])[0],
+                               rtol=0, atol=1e-12)
 
 
 def test_measure_stream_bandwidth():

@@ -26,13 +26,14 @@ import os
 import sys
 
 BP1, BP35, BP3 = 10, 35, 30
+INTERP = 11  # element helpers (hx_interp.cu): BP1.0's former (s, r, t) stage order
 TARGET_THREADS = 256
 
 
 def lines(d, pat):
     d0, d1, d2 = d
-    return {0: (d1 * d2, d0), 1: (d0 * d2, d1), 2: (d0 * d1, d2), 5: (d0 * d1, d2),
-            6: (d0 * d1, d2), 7: (d0 * d2, d1)}[pat]
+    return {0: (d1 * d2, d0), 1: (d0 * d2, d1), 2: (d0 * d1, d2), 4: (d0 * d2, d1),
+            5: (d0 * d1, d2), 6: (d0 * d1, d2), 7: (d0 * d2, d1)}[pat]
 
 
 def kofs(lay, k):
@@ -65,6 +66,9 @@ def addr(d, lay, pat, l, t):
         return kofs(lay, k) + t * s1 + i
     if pat == 7:
         k, i = pair_coords(l, d0, d2)
+        return kofs(lay, k) + t * s1 + i
+    if pat == 4:
+        i, k = divmod(l, d0)
         return kofs(lay, k) + t * s1 + i
     if pat == 2:
         k, j = divmod(l, d1)
@@ -107,7 +111,7 @@ _CACHE_PATH = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__fil
 _cache = None
 
 
-def best_layout(d, pats, paired=False):
+def best_layout(d, pats, paired=False, wide=False):
     """Cheapest layout for one tensor phase (memoised in build/ -- the paired
     search evaluates ~1000 candidates)."""
     global _cache
@@ -117,19 +121,22 @@ def best_layout(d, pats, paired=False):
                 _cache = json.load(fh)
         except (OSError, ValueError):
             _cache = {}
-    key = repr((tuple(d), tuple(pats), bool(paired)))
+    key = repr((tuple(d), tuple(pats), bool(paired))) + (" wide" if wide else "")
     if key not in _cache:
-        _cache[key] = list(_best_layout(d, pats, paired))
+        _cache[key] = list(_best_layout(d, pats, paired, wide))
         os.makedirs(os.path.dirname(_CACHE_PATH), exist_ok=True)
         with open(_CACHE_PATH, "w") as fh:
             json.dump(_cache, fh)
     return tuple(_cache[key])
 
 
-def _best_layout(d, pats, paired=False):
+def _best_layout(d, pats, paired=False, wide=False):
+    """wide: row strides up to d2 + 16 (BP1.0's Y needs s1 = 1 mod 16 with
+    c-fastest j-lines, i.e. 17 at N=7; registers, not shared memory, bound
+    its occupancy)."""
     d0, d1, d2 = d
     best = None
-    for s1 in range(d2, d2 + 4):
+    for s1 in range(d2, d2 + (17 if wide else 4)):
         if not paired:
             cands = ((s0, s1, 0) for s0 in range(d1 * s1, d1 * s1 + 16))
         else:
@@ -149,6 +156,19 @@ def phases(bp, n, m, ord_=0):
         return [(0, (n, n, n), (0, 1, 2)), (1, (n, n, n), (0, 2)),
                 (2, (n, n, n), (0, 1))]
     if bp == BP1:
+        # t-first stage order (hx_bp1.cu): X = (m, n, n) after the t
+        # interpolation, read / written as k-lines by the HBM stages (pattern
+        # 0: coalesced q loads and out stores) and as j-lines by S2 / S4;
+        # Y = (m, m, n), j-lines and i-lines (S3, lanes (c, b) b fastest: the
+        # GwJ loads of S3 are coalesced over that order).  ORD: lane order of
+        # the j-line stages: 0 i fastest (pattern 1), 2 c fastest (4), 4
+        # c-paired (7, with c-paired layouts).  With c fastest the address of
+        # line L is congruent to a multiple of L mod 16 in every stage when
+        # X = (73, 8) and Y = (153, 17) at N=7 (ncu r2_03: the i-fastest /
+        # c-paired orders left 1.7x wavefronts in S3 or in S2 / S4).
+        pj = {0: 1, 2: 4, 4: 7}[ord_]
+        return [(0, (m, n, n), (0, pj)), (1, (m, m, n), (pj, 2))]
+    if bp == INTERP:
         # ORD: lane order of the i-line stages (S2, S4): 0 a fastest (pattern
         # 2), 2 k fastest (5), 4 k-paired (6, with k-paired layouts).  The
         # j-line and k-line stages also touch HBM and keep their coalesced
@@ -187,18 +207,19 @@ def plan(bp, deg, target=TARGET_THREADS, qstage=False):
     lmax = n * n if bp == BP35 else m * m
     epb = max(1, target // lmax)
     nt = -(-epb * lmax // 32) * 32
-    if bp == BP1 and target < lmax and target <= 128:
+    if bp in (BP1, INTERP) and target < lmax and target <= 128:
         # BP1.0 only: a CTA smaller than one element's line count walks over
         # the lines (for_lines); one element per tile
         nt = max(32, -(-target // 32) * 32)
     # BP3.0 supports ORD 4 too, but it measured 1-2 % slower at N=7 despite
     # fewer conflicts (r11/r12: latency-bound, not shared-memory-bound), so
     # the search stays on the default order there
-    ords = {BP1: (0, 2, 4)}.get(bp, (0,))
+    ords = {BP1: (0, 2, 4), INTERP: (0, 2, 4)}.get(bp, (0,))
     best = None
     for o in ords:  # BP1.0: lane orders chosen jointly with the strides
         ph_o = phases(bp, n, m, o)
-        lays_o = [best_layout(d, pats, paired=(6 in pats or 7 in pats)) for _, d, pats in ph_o]
+        lays_o = [best_layout(d, pats, paired=(6 in pats or 7 in pats), wide=(bp == BP1))
+                  for _, d, pats in ph_o]
         c = sum(cost(d, lay, pats, 1, 0) for (_, d, pats), lay in zip(ph_o, lays_o))
         if best is None or c < best[0]:
             best = (c, o, ph_o, lays_o)
@@ -207,7 +228,7 @@ def plan(bp, deg, target=TARGET_THREADS, qstage=False):
     base = [0] * nbuf
     for (b, d, _), lay in zip(ph, lays):
         base[b] = max(base[b], max(extent(d, lay), d[0] * lay[0] if lay[2] == 0 else 0))
-    qs = q_stage_stride(n) if (bp == BP1 and qstage) else 0
+    qs = q_stage_stride(n) if (bp == INTERP and qstage) else 0
     # keep the tile inside the 227 KB shared-memory limit
     while epb > 1 and epb * (sum(base) + 16 * nbuf + n * qs) * 8 > 227 * 1024:
         epb -= 1
@@ -251,15 +272,17 @@ def main(path, policy=None, verbose=False):
            "  }",
            "};", "",
            "template <int BP, int N> struct Cfg;", ""]
-    for bp in (BP1, BP35, BP3):
+    for bp in (BP1, BP35, BP3, INTERP):
         for deg in range(1, 16):
-            target, minb, qst = policy.get((bp, deg),
-                                           (TARGET_THREADS, min_blocks(bp, deg), 0))
+            # the element helpers keep the shape policy tuned for the BP1.0
+            # stage structure they share
+            pol = policy.get((bp, deg)) or (policy.get((BP1, deg)) if bp == INTERP else None)
+            target, minb, qst = pol or (TARGET_THREADS, min_blocks(bp, deg), 0)
             n, m, epb, nt, ph, lays, ebufs, qs, ord_ = plan(bp, deg, target, bool(qst))
             out.append(f"template <> struct Cfg<{bp}, {deg}> {{")
             out.append(f"  static constexpr int EPB = {epb}, NT = {nt}, MINB = {minb};")
             out.append(f"  static constexpr int QS = {qs};  // TMA q-staging slab stride (0: off)")
-            out.append(f"  static constexpr int ORD = {ord_};  // BP1.0 i-line lane order: 0, 2 k-fast, 4 k-paired")
+            out.append(f"  static constexpr int ORD = {ord_};  // lane order (gen_layouts.phases): 0 default, 2 k-fast, 4 paired")
             out.append("  static constexpr int EBUF[%d] = {%s};" % (
                 len(ebufs), ", ".join(str(e) for e in ebufs)))
             out.append("  static constexpr Lay L[%d] = {%s};" % (
