@@ -46,6 +46,21 @@
 #define HX_MINB_BP3_OF(N) Cfg<kBP3, N>::MINB
 #endif
 
+// Diagnostic builds only (numerically wrong, timing only): HX_EXP_NOQ reads
+// q, HX_EXP_NOW the factors, from the first 8 elements (L2-resident), and
+// HX_EXP_NOSTORE drops the output writes, so the kernel runs without that
+// HBM stream.
+#ifdef HX_EXP_NOQ
+#define HX_QEL(e) ((e) & 7)
+#else
+#define HX_QEL(e) (e)
+#endif
+#ifdef HX_EXP_NOW
+#define HX_WEL(e) ((e) & 7)
+#else
+#define HX_WEL(e) (e)
+#endif
+
 namespace hx {
 
 template <int N>
@@ -88,7 +103,7 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT, HX_MINB_BP3_OF(N))
   if (tid == 0 && blockIdx.x < ntiles) {
     const int64_t e0 = int64_t(blockIdx.x) * EPB;
     const int64_t ne = min64(EPB, p.n_el - e0);
-    prefetch_l2(p.q + e0 * n3, ne * n3 * sizeof(double));
+    prefetch_l2(p.q + HX_QEL(e0) * n3, ne * n3 * sizeof(double));
   }
 
   const int el_a = tid / n2, ln_a = tid % n2;
@@ -108,10 +123,10 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT, HX_MINB_BP3_OF(N))
     double* const Cc = Cs + el_c * EC;
 
     // ---- S1: j-lines (k, i): interpolate along s
-    if (HX_PF_BP3 == 1 && tid == 0) prefetch_l2(p.fac + e0 * fs, ne * fs * sizeof(double));
+    if (HX_PF_BP3 == 1 && tid == 0) prefetch_l2(p.fac + HX_WEL(e0) * fs, ne * fs * sizeof(double));
     if (el_a < ne) {
       const int k = ln_a / n, i = ln_a % n;
-      const double* src = p.q + (e0 + el_a) * n3 + k * n2 + i;
+      const double* src = p.q + HX_QEL(e0 + el_a) * n3 + k * n2 + i;
       double x[n], y[m];
 #pragma unroll
       for (int t = 0; t < n; ++t) x[t] = src[t * n];
@@ -124,7 +139,7 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT, HX_MINB_BP3_OF(N))
     }
     __syncthreads();
     // ---- S2: i-lines (k, a): interpolate along r
-    if (HX_PF_BP3 == 2 && tid == 0) prefetch_l2(p.fac + e0 * fs, ne * fs * sizeof(double));
+    if (HX_PF_BP3 == 2 && tid == 0) prefetch_l2(p.fac + HX_WEL(e0) * fs, ne * fs * sizeof(double));
     if (el_b < ne) {
       int k, a;
       iline_coords<n, m, C::ORD>(ln_b, k, a);
@@ -139,12 +154,24 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT, HX_MINB_BP3_OF(N))
     }
     __syncthreads();
     // ---- S3: k-lines (a, c): interpolate along t
-    if (HX_PF_BP3 == 3 && tid == 0) prefetch_l2(p.fac + e0 * fs, ne * fs * sizeof(double));
-    double acc[m];
+    if (HX_PF_BP3 == 3 && tid == 0) prefetch_l2(p.fac + HX_WEL(e0) * fs, ne * fs * sizeof(double));
+    // kAccS (Cfg::ACCS, high degrees): S5's accumulator is parked in the
+    // thread's own, already consumed T k-line instead of staying live in
+    // registers across S6; Z then shares T's layout, so S7 overwrites the
+    // same line in place.
+    constexpr bool kAccS = C::ACCS != 0;
+    // kSerial (Cfg::SER): S4 / S6 finish one line before loading the other,
+    // bounding the live registers to one line.
+    constexpr bool kSerial = C::SER != 0;
+    static_assert(!kAccS || (LZ.s0 == LT.s0 && LZ.s1 == LT.s1 && LZ.sq == LT.sq),
+                  "ACCS needs Z to alias T's layout (tools/gen_layouts.py)");
+    double acc[kAccS ? 1 : m];
     constexpr bool kReread = N >= HX_BP3_REREAD_MIN_N;
     double tvc[kReread ? 1 : m], ttc[kReread ? 1 : m];  // carried S3 -> S5 unless kReread
     const bool act_c = el_c < ne;
     const int ca = ln_c / m, cc = ln_c % m;
+    const double* const gfac = p.fac + HX_WEL(e0 + el_c) * fs + ln_c;
+    auto fac_at = [&](int t, int sl) -> double { return gfac[t * m2 + sl * ss]; };
     if (act_c) {
       const double* src = Bc + ca * LY.s1 + cc;
       double x[n], tv[m];
@@ -162,7 +189,7 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT, HX_MINB_BP3_OF(N))
     }
     __syncthreads();
     // ---- S4: r- and s-derivatives of T
-    if (HX_PF_BP3 == 4 && tid == 0) prefetch_l2(p.fac + e0 * fs, ne * fs * sizeof(double));
+    if (HX_PF_BP3 == 4 && tid == 0) prefetch_l2(p.fac + HX_WEL(e0) * fs, ne * fs * sizeof(double));
     if (act_c) {
       const int kk = ln_c / m, r = ln_c % m;
       double x[m], y[m];
@@ -173,6 +200,7 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT, HX_MINB_BP3_OF(N))
       double* dst = Ac + LQR.kofs(kk) + r * LQR.s1;
 #pragma unroll
       for (int t = 0; t < m; ++t) dst[t] = y[t];
+      if constexpr (kSerial) asm volatile("" ::: "memory");  // one line live at a time
       src = Cc + LT.kofs(kk) + r;  // j-line (kk, c=r)
 #pragma unroll
       for (int t = 0; t < m; ++t) x[t] = src[t * LT.s1];
@@ -183,10 +211,46 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT, HX_MINB_BP3_OF(N))
     }
     __syncthreads();
     // ---- S5: chain rule on k-lines (a, c)
-    if (act_c) {
+    if constexpr (kAccS) {
+      // lean form: only D~_t t and rqt stay in registers; t is re-read point
+      // by point from the thread's own T line, which then takes lam GwJ t
+      // and finally the accumulator
+      static_assert(!kAccS || kReread, "ACCS re-reads T");
+      if (act_c) {
+        double* qrl = Ac + ca * LQR.s1 + cc;
+        double* qsl = Bc + ca * LQS.s1 + cc;
+        double* tl = Cc + ca * LT.s1 + cc;
+        double tt[m], rqt[m];
+        {
+          double tv[m];
+#pragma unroll
+          for (int t = 0; t < m; ++t) tv[t] = tl[LT.kofs(t)];
+          fold_apply<m, m, -1>(p.D, tv, tt);
+        }
+#pragma unroll
+        for (int t = 0; t < m; ++t) {
+          const double grr = fac_at(t, 0), grs = fac_at(t, 1), grt = fac_at(t, 2);
+          const double gss = fac_at(t, 3), gst = fac_at(t, 4), gtt = fac_at(t, 5);
+          const double gwj = fac_at(t, 6);
+          const double qr = qrl[LQR.kofs(t)], qs = qsl[LQS.kofs(t)], qt = tt[t];
+          const double tvt = tl[LT.kofs(t)];
+          const double rqr = grr * qr + grs * qs + grt * qt;
+          const double rqs = grs * qr + gss * qs + gst * qt;
+          qrl[LQR.kofs(t)] = rqr;
+          qsl[LQS.kofs(t)] = rqs;
+          rqt[t] = grt * qr + gst * qs + gtt * qt;
+          const double lt = p.lam * gwj * tvt;
+          if constexpr (ENERGY) en += qr * rqr + qs * rqs + qt * rqt[t] + tvt * lt;
+          tl[LT.kofs(t)] = lt;
+        }
+        double ac[m];
+        fold_apply<m, m, -1>(p.Dt, rqt, ac);
+#pragma unroll
+        for (int t = 0; t < m; ++t) tl[LT.kofs(t)] += ac[t];
+      }
+    } else if (act_c) {
       double* qrl = Ac + ca * LQR.s1 + cc;
       double* qsl = Bc + ca * LQS.s1 + cc;
-      const double* g = p.fac + (e0 + el_c) * fs + ln_c;
       double rqt[m], tv[m], tt[m];
       if constexpr (kReread) {
         // re-read this thread's own T k-line (still intact in C)
@@ -203,10 +267,9 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT, HX_MINB_BP3_OF(N))
       }
 #pragma unroll
       for (int t = 0; t < m; ++t) {
-        const double* gk = g + t * m2;
-        const double grr = gk[0], grs = gk[ss], grt = gk[2 * ss];
-        const double gss = gk[3 * ss], gst = gk[4 * ss], gtt = gk[5 * ss];
-        const double gwj = gk[6 * ss];
+        const double grr = fac_at(t, 0), grs = fac_at(t, 1), grt = fac_at(t, 2);
+        const double gss = fac_at(t, 3), gst = fac_at(t, 4), gtt = fac_at(t, 5);
+        const double gwj = fac_at(t, 6);
         const double qr = qrl[LQR.kofs(t)], qs = qsl[LQS.kofs(t)], qt = tt[t];
         const double rqr = grr * qr + grs * qs + grt * qt;
         const double rqs = grs * qr + gss * qs + gst * qt;
@@ -228,7 +291,7 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT, HX_MINB_BP3_OF(N))
       const int64_t nt = tile + gridDim.x;
       if (nt < ntiles) {
         const int64_t f0 = nt * EPB;
-        prefetch_l2(p.q + f0 * n3, min64(EPB, p.n_el - f0) * n3 * sizeof(double));
+        prefetch_l2(p.q + HX_QEL(f0) * n3, min64(EPB, p.n_el - f0) * n3 * sizeof(double));
       }
     }
     if (act_c) {
@@ -240,6 +303,7 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT, HX_MINB_BP3_OF(N))
       fold_apply<m, m, -1>(p.Dt, x, y);
 #pragma unroll
       for (int t = 0; t < m; ++t) l[t] = y[t];
+      if constexpr (kSerial) asm volatile("" ::: "memory");
       l = Bc + LQS.kofs(kk) + r;
 #pragma unroll
       for (int t = 0; t < m; ++t) x[t] = l[t * LQS.s1];
@@ -252,10 +316,17 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT, HX_MINB_BP3_OF(N))
     if (act_c) {
       const double* qrl = Ac + ca * LQR.s1 + cc;
       const double* qsl = Bc + ca * LQS.s1 + cc;
+      double sum[m];
+      if constexpr (kAccS) {
+        const double* al = Cc + ca * LT.s1 + cc;
 #pragma unroll
-      for (int t = 0; t < m; ++t) acc[t] += qrl[LQR.kofs(t)] + qsl[LQS.kofs(t)];
+        for (int t = 0; t < m; ++t) sum[t] = al[LT.kofs(t)] + qrl[LQR.kofs(t)] + qsl[LQS.kofs(t)];
+      } else {
+#pragma unroll
+        for (int t = 0; t < m; ++t) sum[t] = acc[t] + qrl[LQR.kofs(t)] + qsl[LQS.kofs(t)];
+      }
       double y[n];
-      fold_apply<n, m, 1>(p.It, acc, y);
+      fold_apply<n, m, 1>(p.It, sum, y);
       double* dst = Cc + ca * LZ.s1 + cc;
 #pragma unroll
       for (int t = 0; t < n; ++t) dst[LZ.kofs(t)] = y[t];
@@ -285,7 +356,12 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT, HX_MINB_BP3_OF(N))
       fold_apply<n, m, 1>(p.It, x, y);
       double* dst = p.out + (e0 + el_a) * n3 + k * n2 + i;
 #pragma unroll
-      for (int t = 0; t < n; ++t) st_stream(dst + t * n, y[t]);
+      for (int t = 0; t < n; ++t) {
+#ifdef HX_EXP_NOSTORE
+        if (y[t] == 1.2345e300)  // never true: keeps the work, drops the HBM writes
+#endif
+          st_stream(dst + t * n, y[t]);
+      }
     }
     __syncthreads();  // A is rewritten by the next tile's S1
   }

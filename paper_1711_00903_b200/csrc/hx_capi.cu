@@ -91,6 +91,19 @@ int cuda_status(cudaError_t err) {
 
 using namespace hx;
 
+namespace hx {
+// NVTX range names per operator ("hx_apply BP1.0", ...)
+static const char* range_name(const hx_plan& P, const char* what) {
+  static const char* names[3][4] = {
+      {"hx_apply BP1.0", "hx_apply_host BP1.0", "hx_apply_baseline BP1.0", "hx_apply_energy BP1.0"},
+      {"hx_apply BP3.5", "hx_apply_host BP3.5", "hx_apply_baseline BP3.5", "hx_apply_energy BP3.5"},
+      {"hx_apply BP3.0", "hx_apply_host BP3.0", "hx_apply_baseline BP3.0", "hx_apply_energy BP3.0"}};
+  const int b = P.bp == HX_BP1 ? 0 : P.bp == HX_BP35 ? 1 : 2;
+  const int w = what[0] == 'a' ? 0 : what[0] == 'h' ? 1 : what[0] == 'b' ? 2 : 3;
+  return names[b][w];
+}
+}  // namespace hx
+
 extern "C" {
 
 int hx_plan_create(int bp, int degree, double lam, const double* interp, const double* diff,
@@ -163,12 +176,14 @@ int hx_geometric_factors(const hx_plan* P, const double* vertices, int64_t n_el,
                          double* factors, int* flag, void* stream) {
   if (!P || n_el < 0) return HX_EINVAL;
   if (n_el > 0 && (!vertices || !factors)) return HX_EINVAL;
+  hx::NvtxRange range("hx_geometric_factors");
   return cuda_status(launch_geometry(*P, vertices, n_el, all_slots, factors, flag,
                                      static_cast<cudaStream_t>(stream)));
 }
 
 int hx_repack_factors(const hx_plan* P, const double* src, int64_t n_el, double* dst,
                       int to_packed, void* stream) {
+  hx::NvtxRange range("hx_repack_factors");
   if (!P || n_el < 0) return HX_EINVAL;
   if (n_el > 0 && (!src || !dst)) return HX_EINVAL;
   return cuda_status(launch_repack(*P, src, n_el, dst, to_packed,
@@ -183,6 +198,7 @@ int hx_apply(const hx_plan* P, const double* q, const double* factors, double* o
   if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(factors) |
        reinterpret_cast<uintptr_t>(out)) & 7)
     return HX_EINVAL;
+  hx::NvtxRange range(hx::range_name(*P, "apply"));
   return cuda_status(launch_apply(*P, q, factors, out, n_el, flag, static_cast<cudaStream_t>(stream)));
 }
 
@@ -208,12 +224,14 @@ int hx_apply_baseline(const hx_plan* P, const double* q, const double* factors, 
   if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(factors) |
        reinterpret_cast<uintptr_t>(out) | reinterpret_cast<uintptr_t>(work)) & 7)
     return HX_EINVAL;
+  hx::NvtxRange range(hx::range_name(*P, "baseline"));
   return cuda_status(launch_baseline(*P, q, factors, out, n_el, static_cast<double*>(work), flag,
                                      static_cast<cudaStream_t>(stream)));
 }
 
 int hx_interp_elements(int degree, const double* interp, int project, const double* src,
                        double* dst, int64_t n_el, int* flag, void* stream) {
+  hx::NvtxRange range("hx_interp_elements");
   if (degree < 1 || degree > 15 || n_el < 0 || !interp) return HX_EINVAL;
   if (project != 0 && project != 1) return HX_EINVAL;
   if (n_el == 0) return HX_OK;
@@ -312,6 +330,7 @@ int hx_apply_host(const hx_plan* Pc, const double* q_host, const double* factors
   if (n_el == 0) return HX_OK;
   if (!q_host || !factors || !out_host || !work) return HX_EINVAL;
   hx_plan* P = const_cast<hx_plan*>(Pc);  // lazily owned pipeline resources
+  hx::NvtxRange range(hx::range_name(*P, "host"));
   std::lock_guard<std::mutex> lock(P->pipe_mu);
   cudaStream_t caller = static_cast<cudaStream_t>(stream);
   cudaError_t err = pipe_setup(P);
@@ -387,6 +406,7 @@ int hx_apply_energy(const hx_plan* P, const double* q, const double* factors, do
   if (!P || n_el < 0 || !partials || !energy) return HX_EINVAL;
   if (n_el > 0 && (!q || !factors || !out)) return HX_EINVAL;
   if (n_partials < hx_energy_partials()) return HX_EINVAL;
+  hx::NvtxRange range(hx::range_name(*P, "energy"));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   cudaError_t err = cudaMemsetAsync(partials, 0, sizeof(double) * n_partials, s);
   if (err == cudaSuccess) err = launch_apply(*P, q, factors, out, n_el, flag, s, partials);
@@ -396,6 +416,7 @@ int hx_apply_energy(const hx_plan* P, const double* q, const double* factors, do
 
 int hx_dot(const double* u, const double* v, int64_t n, double* partials, int64_t n_partials,
            double* result, void* stream) {
+  hx::NvtxRange range("hx_dot");
   if (n < 0 || !partials || !result || (n > 0 && (!u || !v))) return HX_EINVAL;
   if (n_partials < hx_energy_partials()) return HX_EINVAL;
   return cuda_status(launch_dot(u, v, n, partials, result, static_cast<cudaStream_t>(stream)));
@@ -404,6 +425,7 @@ int hx_dot(const double* u, const double* v, int64_t n, double* partials, int64_
 int hx_cg_update(double* x, const double* p, double* r, const double* ap, int64_t n,
                  const double* rr, const double* pap, double* partials, int64_t n_partials,
                  double* rr_new, void* stream) {
+  hx::NvtxRange range("hx_cg_update");
   if (n < 0 || !rr || !pap || !partials || !rr_new) return HX_EINVAL;
   if (n > 0 && (!x || !p || !r || !ap)) return HX_EINVAL;
   if (n_partials < hx_energy_partials()) return HX_EINVAL;
@@ -413,6 +435,7 @@ int hx_cg_update(double* x, const double* p, double* r, const double* ap, int64_
 
 int hx_cg_direction(double* p, const double* r, int64_t n, const double* rr_new,
                     const double* rr_old, void* stream) {
+  hx::NvtxRange range("hx_cg_direction");
   if (n < 0 || !rr_new || !rr_old || (n > 0 && (!p || !r))) return HX_EINVAL;
   return cuda_status(launch_cg_direction(p, r, n, rr_new, rr_old,
                                          static_cast<cudaStream_t>(stream)));
@@ -426,6 +449,7 @@ static bool dss_args_ok(int side, int degree, int64_t e_begin, int64_t e_end) {
 
 int hx_dss(const double* in, double* out, int side, int degree, int mask, int64_t e_begin,
            int64_t e_end, int64_t in_base, void* stream) {
+  hx::NvtxRange range("hx_dss");
   if (!dss_args_ok(side, degree, e_begin, e_end) || in_base < 0 || in_base > e_begin)
     return HX_EINVAL;
   if (e_end == e_begin) return HX_OK;
@@ -437,6 +461,7 @@ int hx_dss(const double* in, double* out, int side, int degree, int mask, int64_
 int hx_dot_dss(const double* u, const double* v, int side, int degree, int64_t e_begin,
                int64_t e_end, double* partials, int64_t n_partials, double* result,
                void* stream) {
+  hx::NvtxRange range("hx_dot_dss");
   if (!dss_args_ok(side, degree, e_begin, e_end) || !partials || !result) return HX_EINVAL;
   if (e_end > e_begin && (!u || !v)) return HX_EINVAL;
   if (n_partials < hx_energy_partials()) return HX_EINVAL;
@@ -446,6 +471,7 @@ int hx_dot_dss(const double* u, const double* v, int side, int degree, int64_t e
 
 int hx_dss_inplace(double* u, int side, int degree, int64_t buf_begin, int64_t buf_end,
                    void* stream) {
+  hx::NvtxRange range("hx_dss_inplace");
   if (!dss_args_ok(side, degree, buf_begin, buf_end)) return HX_EINVAL;
   if (buf_end > buf_begin && !u) return HX_EINVAL;
   return cuda_status(launch_dss_inplace(u, side, degree, buf_begin, buf_end,
@@ -456,6 +482,7 @@ int hx_cg_update_assembled(double* x, const double* p, double* r, double* ap, in
                            int degree, int mask, int64_t e_begin, int64_t e_end, int64_t ap_base,
                            int64_t ap_end, const double* rr, const double* pap, double* partials,
                            int64_t n_partials, double* rr_new, void* stream) {
+  hx::NvtxRange range("hx_cg_update_assembled");
   if (!dss_args_ok(side, degree, e_begin, e_end) || ap_base < 0 || ap_base > e_begin ||
       ap_end < e_end || ap_end > int64_t(side) * side * side)
     return HX_EINVAL;

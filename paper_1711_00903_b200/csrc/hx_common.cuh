@@ -16,6 +16,7 @@
 #include <atomic>
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: no-ops unless a profiler injects
 
 // tuning builds substitute an alternative generated table
 #ifdef HX_LAYOUTS_FILE
@@ -167,6 +168,15 @@ __device__ __forceinline__ uint64_t l2_evict_first_policy() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   return pol;
 }
+
+// Host-side NVTX range over one C-ABI call (SURVEY.md §5 tracing): visible in
+// nsys / ncu timelines, ~free when no tool is attached.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 __host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
 

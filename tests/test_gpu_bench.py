@@ -45,7 +45,9 @@ def test_bench_line_contract():
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert d["cpu_baseline"]["kind"] in ("port", "reference") and d["cpu_baseline"]["cores"] >= 1
     assert d["gpu_launches"] >= 3
-    assert d["cpu_baseline"]["kind"] == "reference"  # baseline/_ref travels with the repo
+    if os.path.isdir(os.path.join(ROOT, "baseline", "_ref", "hexbench")):
+        # the installed reference travels with the snapshot (tools/install_reference.sh)
+        assert d["cpu_baseline"]["kind"] == "reference"
     assert d["e2e"]["api"]["value"] > 0
     # per_bp is the line's LAST key (the driver keeps the tail) and slim
     assert list(d)[-1] == "per_bp"

@@ -24,14 +24,16 @@ def parse_header():
     pat = re.compile(
         r"struct Cfg<(\d+), (\d+)> \{\s*static constexpr int EPB = (\d+), NT = (\d+), MINB = (\d+);"
         r"\s*static constexpr int QS = (\d+);[^\n]*\n\s*static constexpr int ORD = (\d+);[^\n]*\n"
+        r"\s*static constexpr int ACCS = (\d+), SER = (\d+);[^\n]*\n"
         r"\s*static constexpr int EBUF\[\d+\] = \{([^}]*)\};\s*static constexpr Lay L\[\d+\] = "
         r"\{(.*?)\};\n\};", re.S)
     for m in pat.finditer(text):
-        bp, deg, epb, nt, minb, qs, ord_ = (int(m.group(i)) for i in range(1, 8))
-        ebuf = [int(x) for x in m.group(8).split(",")]
+        bp, deg, epb, nt, minb, qs, ord_, accs, ser = (int(m.group(i)) for i in range(1, 10))
+        ebuf = [int(x) for x in m.group(10).split(",")]
         lays = [tuple(int(v) for v in t.split(",")) for t in re.findall(r"\{([^{}]*)\}",
-                                                                       m.group(9))]
-        cfgs[(bp, deg)] = dict(epb=epb, nt=nt, minb=minb, qs=qs, ord=ord_, ebuf=ebuf, lays=lays)
+                                                                       m.group(11))]
+        cfgs[(bp, deg)] = dict(epb=epb, nt=nt, minb=minb, qs=qs, ord=ord_, accs=accs,
+                               ser=ser, ebuf=ebuf, lays=lays)
     return cfgs
 
 
@@ -62,4 +64,7 @@ def test_layout_injective_in_bounds_and_fits(key):
         assert max(seen) < c["ebuf"][buf], (key, dims, lay, c["ebuf"][buf])
     smem = sum(c["ebuf"]) * c["epb"] * 8 + (c["epb"] * n * c["qs"] * 8 + 16 if c["qs"] else 0)
     assert smem <= 227 * 1024, (key, smem)
+    if c["accs"]:  # BP3.0: Z is written in place over T's k-lines
+        assert bp == 30 and c["lays"][5] == c["lays"][4], key
+    assert (c["ser"] == 0 and c["accs"] == 0) or bp == 30, key
     assert c["nt"] % 32 == 0 and 32 <= c["nt"] <= 1024

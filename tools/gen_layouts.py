@@ -30,6 +30,20 @@ INTERP = 11  # element helpers (hx_interp.cu): BP1.0's former (s, r, t) stage or
 TARGET_THREADS = 256
 
 
+def _degrees(env, default):
+    v = os.environ.get(env)
+    return default if v is None else {int(x) for x in v.split(",") if x.strip()}
+
+
+# BP3.0 degrees whose S5 accumulator goes through shared memory (Z aliases
+# T's layout; hx_bp3.cu kAccS) -- frees m doubles of registers across S6 --
+# and whose S4 / S6 finish one line before loading the other (kSerial).
+# Measured per degree (profiles/r2_10_bp3_high_degree.md): they pay where
+# the register file, not shared memory, caps the resident CTAs.
+BP3_ACCS = _degrees("HX_GEN_BP3_ACCS", {10, 12, 13, 15})
+BP3_SER = _degrees("HX_GEN_BP3_SER", {10, 12, 13})
+
+
 def lines(d, pat):
     d0, d1, d2 = d
     return {0: (d1 * d2, d0), 1: (d0 * d2, d1), 2: (d0 * d1, d2), 4: (d0 * d2, d1),
@@ -224,6 +238,11 @@ def plan(bp, deg, target=TARGET_THREADS, qstage=False):
         if best is None or c < best[0]:
             best = (c, o, ph_o, lays_o)
     _, ord_, ph, lays = best
+    accs = int(bp == BP3 and deg in BP3_ACCS)
+    ser = int(bp == BP3 and deg in BP3_SER)
+    if accs:
+        lays = list(lays)
+        lays[5] = lays[4]  # Z written in place over T's k-lines
     nbuf = 1 + max(b for b, _, _ in ph)
     base = [0] * nbuf
     for (b, d, _), lay in zip(ph, lays):
@@ -242,7 +261,7 @@ def plan(bp, deg, target=TARGET_THREADS, qstage=False):
             if best is None or c < best[0]:
                 best = (c, eb)
         ebufs.append(best[1])
-    return n, m, epb, nt, ph, lays, ebufs, qs, ord_
+    return n, m, epb, nt, ph, lays, ebufs, qs, ord_, accs, ser
 
 
 def min_blocks(bp, deg):
@@ -278,11 +297,12 @@ def main(path, policy=None, verbose=False):
             # stage structure they share
             pol = policy.get((bp, deg)) or (policy.get((BP1, deg)) if bp == INTERP else None)
             target, minb, qst = pol or (TARGET_THREADS, min_blocks(bp, deg), 0)
-            n, m, epb, nt, ph, lays, ebufs, qs, ord_ = plan(bp, deg, target, bool(qst))
+            n, m, epb, nt, ph, lays, ebufs, qs, ord_, accs, ser = plan(bp, deg, target, bool(qst))
             out.append(f"template <> struct Cfg<{bp}, {deg}> {{")
             out.append(f"  static constexpr int EPB = {epb}, NT = {nt}, MINB = {minb};")
             out.append(f"  static constexpr int QS = {qs};  // TMA q-staging slab stride (0: off)")
             out.append(f"  static constexpr int ORD = {ord_};  // lane order (gen_layouts.phases): 0 default, 2 k-fast, 4 paired")
+            out.append(f"  static constexpr int ACCS = {accs}, SER = {ser};  // BP3.0: S5 accumulator via shared memory (Z aliases T); serial S4/S6 lines")
             out.append("  static constexpr int EBUF[%d] = {%s};" % (
                 len(ebufs), ", ".join(str(e) for e in ebufs)))
             out.append("  static constexpr Lay L[%d] = {%s};" % (
