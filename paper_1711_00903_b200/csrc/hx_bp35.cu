@@ -32,14 +32,6 @@
 #define HX_MINB_BP35_OF(N) Cfg<kBP35, N>::MINB
 #endif
 
-// HX_MINB_BP35 overrides Cfg<>::MINB (resident CTAs per SM for the register
-// budget) in tuning builds only.
-#ifdef HX_MINB_BP35
-#define HX_MINB_BP35_OF(N) HX_MINB_BP35
-#else
-#define HX_MINB_BP35_OF(N) Cfg<kBP35, N>::MINB
-#endif
-
 namespace hx {
 
 template <int N>

@@ -42,6 +42,11 @@ def _degrees(env, default):
 # the register file, not shared memory, caps the resident CTAs.
 BP3_ACCS = _degrees("HX_GEN_BP3_ACCS", {10, 12, 13, 15})
 BP3_SER = _degrees("HX_GEN_BP3_SER", {10, 12, 13})
+# BP3.0 degrees whose layouts weight each access pattern by the number of
+# passes that use it (phases()) instead of counting every pattern once
+# (r2_16: N=10 0.687 -> 0.706, N=12 0.598 -> 0.613, equal elsewhere; at
+# N <= 9 the weighted search returns the unweighted layouts).
+BP3_WEIGHTED = _degrees("HX_GEN_BP3_WEIGHTED", set(range(10, 16)))
 
 
 def lines(d, pat):
@@ -94,8 +99,11 @@ def addr(d, lay, pat, l, t):
 
 
 def cost(d, lay, pats, epb, ebuf):
+    """Modelled wavefronts; a pattern may carry a weight, (pattern, accesses
+    per element relative to one pass)."""
     total = 0
-    for pat in pats:
+    for pw in pats:
+        pat, w = pw if isinstance(pw, tuple) else (pw, 1)
         nl, ln = lines(d, pat)
         tot_lines = nl * epb
         for w0 in range(0, tot_lines, 32):
@@ -110,7 +118,7 @@ def cost(d, lay, pats, epb, ebuf):
                     cnt = [0] * 16
                     for a in words:
                         cnt[a & 15] += 1
-                    total += max(cnt)
+                    total += w * max(cnt)
     return total
 
 
@@ -194,6 +202,17 @@ def phases(bp, n, m, ord_=0):
     # theirs: with odd m the unpaired last slice costs more than it saves
     # (r11: 1.3-1.5x wavefronts there with pattern 6 / 7).
     pi = 6 if ord_ == 4 else 2
+    if n - 1 in BP3_WEIGHTED:
+        # patterns weighted by the passes each tensor sees (hx_bp3.cu): X is
+        # written in S1 and S8, read in S2 and S9; QR / QS are read and
+        # written by S5, read by S7 (k-lines) and touched three times by
+        # S4 / S6 (i- resp. j-lines); T is written by S3 and read by S4 both
+        # ways and by S5 (with ACCS also re-read, rewritten twice and read
+        # by S7 -- ACCS degrees are searched jointly with Z, see plan())
+        wt = 7 if n - 1 in BP3_ACCS else 2
+        return [(0, (n, m, n), ((1, 2), (pi, 2))), (0, (m, m, m), ((0, 3), (2, 3))),
+                (1, (n, m, m), ((0, 1), (pi, 1))), (1, (m, m, m), ((0, 3), (1, 3))),
+                (2, (m, m, m), ((0, wt), (1, 1), (2, 1))), (2, (n, m, m), ((0, 1), (pi, 1)))]
     return [(0, (n, m, n), (1, pi)), (0, (m, m, m), (0, 2)),
             (1, (n, m, m), (0, pi)), (1, (m, m, m), (0, 1)),
             (2, (m, m, m), (0, 1, 2)), (2, (n, m, m), (0, pi))]
@@ -242,6 +261,14 @@ def plan(bp, deg, target=TARGET_THREADS, qstage=False):
     ser = int(bp == BP3 and deg in BP3_SER)
     if accs:
         lays = list(lays)
+        if deg in BP3_WEIGHTED:
+            # one layout for T and Z (Z written in place over T's k-lines)
+            (_, dt, pt), (_, dz, pz) = ph[4], ph[5]
+            d0, d1, d2 = dt
+            cands = [(s0_, s1_, 0) for s1_ in range(d2, d2 + 4)
+                     for s0_ in range(d1 * s1_, d1 * s1_ + 16)]
+            lays[4] = min(cands, key=lambda l: (cost(dt, l, pt, 1, 0) + cost(dz, l, pz, 1, 0),
+                                                extent(dt, l)))
         lays[5] = lays[4]  # Z written in place over T's k-lines
     nbuf = 1 + max(b for b, _, _ in ph)
     base = [0] * nbuf
