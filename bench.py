@@ -446,11 +446,18 @@ def reference_cpu(seconds=3.0):
             "port": {k: port[k] for k in ("value", "cores", "kind", "sample")}}
 
 
+E2E_CHUNK_BYTES = 64 << 20  # uniform pipeline chunks for back-to-back steps (tune28)
+
+
 def e2e_report(op, mesh, steps, warmup):
-    """Same metric through the public host-buffer API (hx_apply_host, the
-    library's default chunking): per step the H2D copy of q from pinned
-    memory, the kernel and the D2H copy of out, each call stream-ordered
-    after the previous one (no cross-call overlap)."""
+    """Same metric through the public host-buffer API: per step the H2D copy
+    of q from pinned memory, the kernel and the D2H copy of out.  Steps are a
+    stream of independent applies, so they use the library's opt-in
+    back-to-back mode (hx_apply_host_ex with HX_HOST_OVERLAP: each call's
+    uploads run under the previous call's downloads; the bench guarantees the
+    mode's contract -- q is final, out is read only after the timed region,
+    the workspace is this operator's).  The stream-ordered default mode (no
+    cross-call overlap) is timed too and reported beside it."""
     import torch
     import paper_1711_00903_b200 as hx
     from paper_1711_00903_b200 import operators
@@ -460,23 +467,35 @@ def e2e_report(op, mesh, steps, warmup):
     q_pin.copy_(torch.from_numpy(np.random.default_rng(0).standard_normal(n)))
     o_pin = torch.empty(n, dtype=torch.float64).pin_memory()
     qh, oh = q_pin.numpy(), o_pin.numpy()
-    chunk = operators.host_chunk_elements(op)
-    work = operators._device_work(op, chunk)
     stream = torch.cuda.current_stream()
-    for _ in range(warmup):
-        hx.apply_host(op, qh, oh, chunk_el=chunk, work=work)
-    torch.cuda.synchronize()
-    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s.record(stream)
-    for _ in range(steps):
-        hx.apply_host(op, qh, oh, chunk_el=chunk, work=work)
-    e.record(stream)
-    e.synchronize()
-    ms = s.elapsed_time(e) / steps
+
+    def timed(chunk, overlap):
+        work = operators._device_work(op, chunk)
+        for _ in range(warmup):
+            hx.apply_host(op, qh, oh, chunk_el=chunk, work=work, overlap=overlap)
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        for _ in range(steps):
+            hx.apply_host(op, qh, oh, chunk_el=chunk, work=work, overlap=overlap)
+        e.record(stream)
+        e.synchronize()
+        del work
+        return s.elapsed_time(e) / steps
+
+    chunk = max(1, E2E_CHUNK_BYTES // (op.n_p * 8))
+    ms = timed(chunk, True)
+    default_chunk = operators.host_chunk_elements(op)
+    ms_ordered = timed(default_chunk, False)
     return ms, {"value": None, "unit": "GDOF/s", "h2d_bytes_per_step": n * 8,
                 "d2h_bytes_per_step": n * 8, "ms_per_step": ms,
-                "path": "hx_apply_host (C ABI), pinned host q/out, chunked 3-stream "
-                        f"H2D/kernel/D2H pipeline, chunk {chunk} elements, stream-ordered calls"}
+                "path": "hx_apply_host_ex (C ABI), pinned host q/out, chunked 3-stream "
+                        f"H2D/kernel/D2H pipeline, {chunk}-element chunks, HX_HOST_OVERLAP "
+                        "(back-to-back steps pipelined)",
+                "stream_ordered": {"value": mesh.n_el * op.n_p / (ms_ordered * 1e-3) / 1e9,
+                                   "ms_per_step": ms_ordered,
+                                   "path": f"hx_apply_host, {default_chunk}-element ramped "
+                                           "chunks, each call after the previous one"}}
 
 
 def e2e_api_report(op, mesh, steps, warmup):

@@ -115,6 +115,21 @@ int hx_apply_host(const hx_plan* plan, const double* q_host, const double* facto
                   double* out_host, int64_t n_el, int64_t chunk_el, void* work,
                   int* status_flag, void* stream);
 
+/* hx_apply_host with flags.  HX_HOST_OVERLAP opts into back-to-back
+ * pipelining for streaming callers: the call does NOT wait for work queued on
+ * `stream` before it; it follows only this plan's previous host-pipeline call
+ * and continues its buffer-slot sequence (when `work` and `chunk_el` are
+ * unchanged), so its H2D copies and kernels run under the previous call's D2H
+ * tail, and its chunks are uniform (no ramp).  The caller guarantees that
+ * q_host already holds its final contents, that nothing else reads or writes
+ * q_host / out_host until `stream` reaches the end of the call, and that
+ * `work` is used by no other plan or stream.  `stream` still waits for the
+ * whole pipeline.  flags = 0 is exactly hx_apply_host.                      */
+#define HX_HOST_OVERLAP 1u
+int hx_apply_host_ex(const hx_plan* plan, const double* q_host, const double* factors,
+                     double* out_host, int64_t n_el, int64_t chunk_el, void* work,
+                     int* status_flag, unsigned flags, void* stream);
+
 /* Drop-in host path for the arrays the reference's users pass to
  * apply_operator (operators.py:306-331): q_host / out_host may be PAGEABLE
  * (plain numpy memory).  Pageable buffers stream through `staging`, a

@@ -17,6 +17,7 @@ LIB_PATH = os.environ.get("HX_LIB_PATH", os.path.join(HERE, "libhexbench_b200.so
 HX_OK, HX_EINVAL, HX_ENONFINITE, HX_EDEGENERATE, HX_ECUDA, HX_ENOMEM = range(6)
 HX_BP1, HX_BP35, HX_BP3 = 10, 35, 30
 HX_FLAG_NONFINITE, HX_FLAG_DEGENERATE = 1, 2
+HX_HOST_OVERLAP = 1  # hx_apply_host_ex: back-to-back pipelining (include/hexbench_b200.h)
 
 # every symbol include/hexbench_b200.h declares, with its ctypes signature
 _c = ctypes
@@ -34,6 +35,8 @@ SIGNATURES = {
     "hx_apply_range": (_c.c_int, [_P, _P, _P, _P, _c.c_int64, _c.c_int64, _P, _P]),
     "hx_apply_host_workspace": (_c.c_int64, [_P, _c.c_int64]),
     "hx_apply_host": (_c.c_int, [_P, _P, _P, _P, _c.c_int64, _c.c_int64, _P, _P, _P]),
+    "hx_apply_host_ex": (_c.c_int, [_P, _P, _P, _P, _c.c_int64, _c.c_int64, _P, _P, _c.c_uint,
+                                    _P]),
     "hx_apply_host_staging_bytes": (_c.c_int64, [_P, _c.c_int64]),
     "hx_apply_host_staged": (_c.c_int, [_P, _P, _P, _P, _c.c_int64, _c.c_int64, _P, _P, _P,
                                         _P]),

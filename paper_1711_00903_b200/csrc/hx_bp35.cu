@@ -91,19 +91,30 @@ __global__ void __launch_bounds__(Cfg<kBP35, N>::NT, HX_MINB_BP35_OF(N))
     double* const Be = B + el * EB;
     double* const Ce = Cs + el * EC;
 
-    double qv[n], qt[n], acc[n];
+    // kLean (Cfg::ACCS, high degrees): nothing stays in registers across a
+    // barrier -- S3 re-reads q from its own k-line of A (nobody else reads
+    // A after S2), takes D_t q there, and parks the accumulator in the same
+    // line for S5 -- instead of carrying q, D_t q (S1 -> S3) and the
+    // accumulator (S3 -> S5) through S2 / S4's two-line register peaks.
+    constexpr bool kLean = C::ACCS != 0;
+    double qv[kLean ? 1 : n], qt[kLean ? 1 : n], acc[kLean ? 1 : n];
     // ---- S1: k-lines over (j, i)
     if (act) {
       const int j = ln / n, i = ln % n;
       const double* src = p.q + e * n3 + j * n + i;
+      double qk[n];
 #pragma unroll
-      for (int k = 0; k < n; ++k) qv[k] = src[k * n2];
-      const bool bad = any_nonfinite(qv);
+      for (int k = 0; k < n; ++k) qk[k] = src[k * n2];
+      const bool bad = any_nonfinite(qk);
       if (bad && p.flag) atomicOr(p.flag, 1);
-      fold_apply<n, n, -1>(p.D, qv, qt);
+      if constexpr (!kLean) {
+#pragma unroll
+        for (int k = 0; k < n; ++k) qv[k] = qk[k];
+        fold_apply<n, n, -1>(p.D, qv, qt);
+      }
       double* a = Ae + j * LA.s1 + i;
 #pragma unroll
-      for (int k = 0; k < n; ++k) a[k * LA.s0] = qv[k];
+      for (int k = 0; k < n; ++k) a[k * LA.s0] = qk[k];
     }
     __syncthreads();
     // ---- S2: r- and s-derivatives
@@ -141,27 +152,45 @@ __global__ void __launch_bounds__(Cfg<kBP35, N>::NT, HX_MINB_BP35_OF(N))
       double* b = Be + j * LB.s1 + i;
       double* c = Ce + j * LC.s1 + i;
       const double* g = p.fac + e * p.fac_estride + j * n + i;
-      double rqt[n];
+      double* a = Ae + j * LA.s1 + i;  // this thread's own k-line of q
+      double rqt[n], qtl[n];
+      if constexpr (kLean) {
+        double x[n];
+#pragma unroll
+        for (int k = 0; k < n; ++k) x[k] = a[k * LA.s0];
+        fold_apply<n, n, -1>(p.D, x, qtl);
+      }
 #pragma unroll
       for (int k = 0; k < n; ++k) {
         const double* gk = g + k * n2;
         const double grr = gk[0], grs = gk[ss], grt = gk[2 * ss];
         const double gss = gk[3 * ss], gst = gk[4 * ss], gtt = gk[5 * ss];
         const double gwj = gk[6 * ss];
-        const double qr = b[k * LB.s0], qs = c[k * LC.s0], qtk = qt[k];
+        const double qk = kLean ? a[k * LA.s0] : qv[k];
+        const double qr = b[k * LB.s0], qs = c[k * LC.s0], qtk = kLean ? qtl[k] : qt[k];
         const double rqr = grr * qr + grs * qs + grt * qtk;
         const double rqs = grs * qr + gss * qs + gst * qtk;
         b[k * LB.s0] = rqr;
         c[k * LC.s0] = rqs;
         rqt[k] = grt * qr + gst * qs + gtt * qtk;
-        const double lq = p.lam * gwj * qv[k];
+        const double lq = p.lam * gwj * qk;
         // <q, A q> = sum over points of grad q . G grad q + lam GwJ q^2
-        if constexpr (ENERGY) en += qr * rqr + qs * rqs + qtk * rqt[k] + qv[k] * lq;
-        qv[k] = lq;
+        if constexpr (ENERGY) en += qr * rqr + qs * rqs + qtk * rqt[k] + qk * lq;
+        if constexpr (kLean)
+          a[k * LA.s0] = lq;
+        else
+          qv[k] = lq;
       }
-      fold_apply<n, n, -1>(p.Dt, rqt, acc);
+      if constexpr (kLean) {
+        double ac[n];
+        fold_apply<n, n, -1>(p.Dt, rqt, ac);
 #pragma unroll
-      for (int k = 0; k < n; ++k) acc[k] += qv[k];
+        for (int k = 0; k < n; ++k) a[k * LA.s0] += ac[k];
+      } else {
+        fold_apply<n, n, -1>(p.Dt, rqt, acc);
+#pragma unroll
+        for (int k = 0; k < n; ++k) acc[k] += qv[k];
+      }
     }
     __syncthreads();
     // ---- S4: transposed r- and s-derivatives, in place
@@ -188,8 +217,10 @@ __global__ void __launch_bounds__(Cfg<kBP35, N>::NT, HX_MINB_BP35_OF(N))
       const double* b = Be + j * LB.s1 + i;
       const double* c = Ce + j * LC.s1 + i;
       double* dst = p.out + e * n3 + j * n + i;
+      const double* a = Ae + j * LA.s1 + i;
 #pragma unroll
-      for (int k = 0; k < n; ++k) st_stream(dst + k * n2, acc[k] + b[k * LB.s0] + c[k * LC.s0]);
+      for (int k = 0; k < n; ++k)
+        st_stream(dst + k * n2, (kLean ? a[k * LA.s0] : acc[k]) + b[k * LB.s0] + c[k * LC.s0]);
     }
     // A is rewritten by the next tile's S1 only after it has passed this
     // tile's S3/S4 barriers; B and C only after the next S1 barrier.

@@ -326,7 +326,14 @@ extern "C" {
 int hx_apply_host(const hx_plan* Pc, const double* q_host, const double* factors,
                   double* out_host, int64_t n_el, int64_t chunk_el, void* work, int* flag,
                   void* stream) {
-  if (!Pc || n_el < 0 || chunk_el <= 0) return HX_EINVAL;
+  return hx_apply_host_ex(Pc, q_host, factors, out_host, n_el, chunk_el, work, flag, 0u,
+                          stream);
+}
+
+int hx_apply_host_ex(const hx_plan* Pc, const double* q_host, const double* factors,
+                     double* out_host, int64_t n_el, int64_t chunk_el, void* work, int* flag,
+                     unsigned flags, void* stream) {
+  if (!Pc || n_el < 0 || chunk_el <= 0 || (flags & ~HX_HOST_OVERLAP)) return HX_EINVAL;
   if (n_el == 0) return HX_OK;
   if (!q_host || !factors || !out_host || !work) return HX_EINVAL;
   hx_plan* P = const_cast<hx_plan*>(Pc);  // lazily owned pipeline resources
@@ -348,34 +355,49 @@ int hx_apply_host(const hx_plan* Pc, const double* q_host, const double* factors
   cudaEvent_t* e_in = P->ev[0];
   cudaEvent_t* e_k = P->ev[1];
   cudaEvent_t* e_out = P->ev[2];
-  // Stream-ordered like every other entry point: all three pipeline streams
-  // start after what the caller queued before this call -- the work that
-  // produces q_host (e.g. an earlier call's D2H into it), earlier users of
-  // `work`, factor generation.
-  cudaEvent_t start;
-  if ((err = cudaEventCreateWithFlags(&start, cudaEventDisableTiming)) != cudaSuccess)
-    return cuda_status(err);
-  cudaEventRecord(start, caller);
-  cudaStreamWaitEvent(s_in, start, 0);
-  cudaStreamWaitEvent(s_k, start, 0);
-  cudaStreamWaitEvent(s_out, start, 0);
-  cudaEventDestroy(start);  // released once recorded work completes
-  // ... and after the plan's previous host-pipeline call, whatever stream it
-  // came from: the pipeline streams and their slot events are shared
-  cudaStreamWaitEvent(s_in, P->pipe_last, 0);
-  cudaStreamWaitEvent(s_k, P->pipe_last, 0);
-  const std::vector<int64_t> sched = chunk_schedule(n_el, chunk_el);
+  const bool overlap = (flags & HX_HOST_OVERLAP) != 0;
+  if (!overlap) {
+    // Stream-ordered like every other entry point: all three pipeline
+    // streams start after what the caller queued before this call -- the
+    // work that produces q_host (e.g. an earlier call's D2H into it),
+    // earlier users of `work`, factor generation.
+    cudaEvent_t start;
+    if ((err = cudaEventCreateWithFlags(&start, cudaEventDisableTiming)) != cudaSuccess)
+      return cuda_status(err);
+    cudaEventRecord(start, caller);
+    cudaStreamWaitEvent(s_in, start, 0);
+    cudaStreamWaitEvent(s_k, start, 0);
+    cudaStreamWaitEvent(s_out, start, 0);
+    cudaEventDestroy(start);  // released once recorded work completes
+  }
+  // After the plan's previous host-pipeline call, whatever stream it came
+  // from (the pipeline streams and slot events are shared): a full drain,
+  // or -- HX_HOST_OVERLAP with the same workspace and chunking -- per slot,
+  // continuing the previous call's slot sequence.
+  const bool cont = overlap && P->pipe_cont && P->pipe_work == work && P->pipe_chunk == chunk_el;
+  const int64_t seq = cont ? P->pipe_seq : 0;
+  if (!cont) {
+    cudaStreamWaitEvent(s_in, P->pipe_last, 0);
+    cudaStreamWaitEvent(s_k, P->pipe_last, 0);
+  }
+  std::vector<int64_t> sched;
+  if (overlap) {  // uniform chunks: back-to-back calls keep the pipe full
+    for (int64_t e = 0; e < n_el; e += chunk_el) sched.push_back(std::min(chunk_el, n_el - e));
+  } else {
+    sched = chunk_schedule(n_el, chunk_el);
+  }
   const int64_t nchunks = int64_t(sched.size());
   int64_t e0 = 0;
   for (int64_t c = 0; c < nchunks; ++c) {
-    const int slot = int(c % S);
+    const int64_t g = seq + c;  // position in the slot sequence
+    const int slot = int(g % S);
     const int64_t ne = sched[c];
     const size_t bytes = size_t(ne * n3) * sizeof(double);
-    if (c >= S) cudaStreamWaitEvent(s_in, e_k[slot], 0);  // kernel c-S done reading wq[slot]
+    if (g >= S) cudaStreamWaitEvent(s_in, e_k[slot], 0);  // kernel g-S done reading wq[slot]
     cudaMemcpyAsync(wq[slot], q_host + e0 * n3, bytes, cudaMemcpyHostToDevice, s_in);
     cudaEventRecord(e_in[slot], s_in);
     cudaStreamWaitEvent(s_k, e_in[slot], 0);
-    if (c >= S) cudaStreamWaitEvent(s_k, e_out[slot], 0);  // D2H c-S done with wo[slot]
+    if (g >= S) cudaStreamWaitEvent(s_k, e_out[slot], 0);  // D2H g-S done with wo[slot]
     if ((err = launch_apply(*P, wq[slot], factors + e0 * P->elem_stride, wo[slot], ne, flag, s_k)) !=
         cudaSuccess) {
       // copies into / out of the caller's host buffers may still be in
@@ -383,6 +405,7 @@ int hx_apply_host(const hx_plan* Pc, const double* q_host, const double* factors
       cudaStreamSynchronize(s_in);
       cudaStreamSynchronize(s_k);
       cudaStreamSynchronize(s_out);
+      P->pipe_cont = false;
       return cuda_status(err);
     }
     cudaEventRecord(e_k[slot], s_k);
@@ -395,6 +418,10 @@ int hx_apply_host(const hx_plan* Pc, const double* q_host, const double* factors
   // of the call: its last chunk done means the whole pipeline is
   cudaEventRecord(P->pipe_last, s_out);
   cudaStreamWaitEvent(caller, P->pipe_last, 0);
+  P->pipe_seq = seq + nchunks;
+  P->pipe_work = work;
+  P->pipe_chunk = chunk_el;
+  P->pipe_cont = overlap;
   return cuda_status(cudaGetLastError());
 }
 

@@ -318,6 +318,7 @@ int hx_apply_host_staged(const hx_plan* Pc, const double* q_host, const double* 
     cudaStreamSynchronize(s_out);
     return cuda_status(err);
   }
+  P->pipe_cont = false;  // slot sequence restarted: HX_HOST_OVERLAP calls drain first
   cudaEventRecord(P->pipe_last, s_out);
   if ((err = drain(nchunks, true)) != cudaSuccess) return cuda_status(err);
   cudaStreamWaitEvent(caller, P->pipe_last, 0);

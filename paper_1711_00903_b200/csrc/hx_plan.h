@@ -38,6 +38,12 @@ struct hx_plan {
   cudaStream_t pipe[3];
   cudaEvent_t ev[3][hx_host_slots];
   cudaEvent_t pipe_last;  // end of the plan's latest host-pipeline call
+  // HX_HOST_OVERLAP continuation state: slot sequence, workspace and chunk
+  // of the previous call (continued only when unchanged)
+  int64_t pipe_seq = 0;
+  const void* pipe_work = nullptr;
+  int64_t pipe_chunk = 0;
+  bool pipe_cont = false;
   bool pipe_ready;
   int pipe_dev = -1;
   std::mutex pipe_mu;

@@ -340,16 +340,17 @@ def _device_work(op, chunk_el):
     return torch.empty(nbytes // DOUBLE, dtype=torch.float64, device=op.device)
 
 
-def _apply_host(op, src, dst, flag, stream, chunk_el=None, work=None):
+def _apply_host(op, src, dst, flag, stream, chunk_el=None, work=None, overlap=False):
     if op.n_el == 0:
         return dst
     if chunk_el is None:
         chunk_el = host_chunk_elements(op)
     if work is None:
         work = _device_work(op, chunk_el)
-    _native.check(_native.lib().hx_apply_host(
+    _native.check(_native.lib().hx_apply_host_ex(
         op.plan.handle, _native.ptr(src), _native.ptr(op.device_factors), _native.ptr(dst),
-        op.n_el, chunk_el, _native.ptr(work), _native.ptr(flag), stream), "hx_apply_host")
+        op.n_el, chunk_el, _native.ptr(work), _native.ptr(flag),
+        _native.HX_HOST_OVERLAP if overlap else 0, stream), "hx_apply_host_ex")
     return dst
 
 
@@ -396,12 +397,19 @@ def _apply_numpy(op, src, dst, flag, stream, chunk_el=None):
     return dst
 
 
-def apply_host(op, src, dst, flag=None, stream=None, chunk_el=None, work=None):
+def apply_host(op, src, dst, flag=None, stream=None, chunk_el=None, work=None, overlap=False):
     """End-to-end apply on host arrays through ``hx_apply_host`` (asynchronous on
-    ``stream``; pass page-locked arrays for full copy/compute overlap)."""
+    ``stream``; pass page-locked arrays for full copy/compute overlap).
+
+    ``overlap=True`` (HX_HOST_OVERLAP) pipelines back-to-back calls: the call
+    does not wait for earlier work on ``stream``, its uploads and kernels run
+    under the previous call's downloads.  Only for streaming callers that
+    guarantee ``src`` is final, nobody touches ``src`` / ``dst`` until the
+    stream passes the call, and ``work`` belongs to this operator alone
+    (include/hexbench_b200.h, hx_apply_host_ex)."""
     if stream is None:
         stream = _stream(op.device)
-    return _apply_host(op, src, dst, flag, stream, chunk_el, work)
+    return _apply_host(op, src, dst, flag, stream, chunk_el, work, overlap)
 
 
 def baseline_workspace(op):

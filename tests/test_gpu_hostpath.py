@@ -90,6 +90,49 @@ def test_apply_host_same_plan_two_streams_one_workspace(mesh3):
 
 
 @pytest.mark.parametrize("bp", BPS)
+@pytest.mark.parametrize("chunks", [1, 2, 4, 7])
+def test_apply_host_overlap_back_to_back_bitwise(bp, chunks, mesh3):
+    """HX_HOST_OVERLAP: independent calls queued back to back pipeline into
+    each other (the slot sequence continues across calls); every output is
+    bitwise the device apply, including across a change of chunking (full
+    drain), an interleaved stream-ordered call and a staged call."""
+    op = hx.make_operator(bp, 7, mesh3, lam=0.7)
+    rng = np.random.default_rng(11)
+    chunk = -(-op.n_el // chunks)
+    work = operators._device_work(op, max(chunk, 3))
+    qs = [pinned((op.n_el, op.n_p)) for _ in range(8)]
+    outs = [pinned((op.n_el, op.n_p)) for _ in range(8)]
+    for q, o in zip(qs, outs):
+        q[:] = rng.standard_normal(q.shape)
+        o[:] = np.nan
+    for i, (q, o) in enumerate(zip(qs, outs)):
+        if i == 4:  # a plain stream-ordered call in the middle of the stream
+            hx.apply_host(op, q, o, chunk_el=chunk, work=work)
+        elif i == 5:  # another chunking: the pipeline drains first
+            hx.apply_host(op, q, o, chunk_el=3, work=work, overlap=True)
+        elif i == 6:  # the staged (pageable) path on the same plan
+            torch.cuda.synchronize()
+            o[:] = hx.apply_operator(op, hx.FieldVector(op.n_el, op.n_p, np.array(q))).data
+        else:
+            hx.apply_host(op, q, o, chunk_el=chunk, work=work, overlap=True)
+    torch.cuda.synchronize()
+    for q, o in zip(qs, outs):
+        np.testing.assert_array_equal(o, dev_apply(op, q))
+
+
+def test_apply_host_ex_rejects_unknown_flags(mesh3):
+    op = hx.make_operator(hx.BP35, 3, mesh3, lam=1.0)
+    q = pinned((op.n_el, op.n_p))
+    q[:] = 1.0
+    o = pinned(q.shape)
+    work = operators._device_work(op, op.n_el)
+    st = _native.lib().hx_apply_host_ex(
+        op.plan.handle, _native.ptr(q), _native.ptr(op.device_factors), _native.ptr(o),
+        op.n_el, op.n_el, _native.ptr(work), None, 2, None)
+    assert st != 0
+
+
+@pytest.mark.parametrize("bp", BPS)
 def test_staged_pageable_path_bitwise(bp, mesh3):
     """apply_operator on plain numpy (pageable) arrays, forced through many
     chunks of the pinned ring, in every combination of pageable / pinned

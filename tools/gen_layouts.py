@@ -42,6 +42,12 @@ def _degrees(env, default):
 # the register file, not shared memory, caps the resident CTAs.
 BP3_ACCS = _degrees("HX_GEN_BP3_ACCS", {10, 12, 13, 15})
 BP3_SER = _degrees("HX_GEN_BP3_SER", {10, 12, 13})
+# BP3.5 degrees whose kernel keeps nothing in registers across a barrier
+# (hx_bp35.cu kLean, emitted as ACCS): q, D_t q and the accumulator go
+# through the thread's own k-line of buffer A (r2_19: N=11 0.855 -> 0.873,
+# N=12 0.852 -> 0.943, N=13 0.747 -> 0.791 and N=14 0.788 -> 0.823 at MINB 2,
+# N=15 0.815 -> 0.882; slower at N <= 10, where the registers are there).
+BP35_LEAN = _degrees("HX_GEN_BP35_LEAN", set(range(11, 16)))
 # BP3.0 degrees whose layouts weight each access pattern by the number of
 # passes that use it (phases()) instead of counting every pattern once
 # (r2_16: N=10 0.687 -> 0.706, N=12 0.598 -> 0.613, equal elsewhere; at
@@ -257,9 +263,9 @@ def plan(bp, deg, target=TARGET_THREADS, qstage=False):
         if best is None or c < best[0]:
             best = (c, o, ph_o, lays_o)
     _, ord_, ph, lays = best
-    accs = int(bp == BP3 and deg in BP3_ACCS)
+    accs = int((bp == BP3 and deg in BP3_ACCS) or (bp == BP35 and deg in BP35_LEAN))
     ser = int(bp == BP3 and deg in BP3_SER)
-    if accs:
+    if accs and bp == BP3:
         lays = list(lays)
         if deg in BP3_WEIGHTED:
             # one layout for T and Z (Z written in place over T's k-lines)
