@@ -6,7 +6,7 @@ OUT=${1:-gpurun_out/sanit}
 mkdir -p "$OUT"
 timeout 2000 compute-sanitizer --tool memcheck --leak-check no --error-exitcode 99 --print-limit 20 \
   python -m pytest tests/test_gpu_parity.py tests/test_gpu_helpers.py tests/test_gpu_assembly.py \
-  tests/test_gpu_cg.py tests/test_gpu_acceptance.py -q -x -p no:cacheprovider \
+  tests/test_gpu_cg.py tests/test_gpu_acceptance.py tests/test_gpu_hostpath.py -q -x -p no:cacheprovider \
   -k "not full_size and not sharded_assembled and not 64bit and not two_ranks and not report_cli" \
   > "$OUT/memcheck.log" 2>&1
 echo "exit $?" >> "$OUT/memcheck.log"
