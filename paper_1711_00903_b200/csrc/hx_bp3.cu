@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT, HX_MINB_BP3_OF(N))
     if (HX_PF_BP3 == 2 && tid == 0) prefetch_l2(p.fac + HX_WEL(e0) * fs, ne * fs * sizeof(double));
     if (el_b < ne) {
       int k, a;
-      iline_coords<n, m, C::ORD>(ln_b, k, a);
+      iline_coords<n, m, (C::ORD & 4)>(ln_b, k, a);
       const double* src = Ab + LX.kofs(k) + a * LX.s1;
       double x[n], y[m];
 #pragma unroll
@@ -191,7 +191,8 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT, HX_MINB_BP3_OF(N))
     // ---- S4: r- and s-derivatives of T
     if (HX_PF_BP3 == 4 && tid == 0) prefetch_l2(p.fac + HX_WEL(e0) * fs, ne * fs * sizeof(double));
     if (act_c) {
-      const int kk = ln_c / m, r = ln_c % m;
+      // ORD bit 8 (even m): the i-line half takes its lines k-fastest
+      const int kk = (C::ORD & 8) ? ln_c % m : ln_c / m, r = (C::ORD & 8) ? ln_c / m : ln_c % m;
       double x[m], y[m];
       const double* src = Cc + LT.kofs(kk) + r * LT.s1;  // i-line (kk, a=r)
 #pragma unroll
@@ -201,11 +202,12 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT, HX_MINB_BP3_OF(N))
 #pragma unroll
       for (int t = 0; t < m; ++t) dst[t] = y[t];
       if constexpr (kSerial) asm volatile("" ::: "memory");  // one line live at a time
-      src = Cc + LT.kofs(kk) + r;  // j-line (kk, c=r)
+      const int kj = ln_c / m, rj = ln_c % m;
+      src = Cc + LT.kofs(kj) + rj;  // j-line (kk, c=r)
 #pragma unroll
       for (int t = 0; t < m; ++t) x[t] = src[t * LT.s1];
       fold_apply<m, m, -1>(p.D, x, y);
-      dst = Bc + LQS.kofs(kk) + r;
+      dst = Bc + LQS.kofs(kj) + rj;
 #pragma unroll
       for (int t = 0; t < m; ++t) dst[t * LQS.s1] = y[t];
     }
@@ -295,7 +297,7 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT, HX_MINB_BP3_OF(N))
       }
     }
     if (act_c) {
-      const int kk = ln_c / m, r = ln_c % m;
+      const int kk = (C::ORD & 8) ? ln_c % m : ln_c / m, r = (C::ORD & 8) ? ln_c / m : ln_c % m;
       double x[m], y[m];
       double* l = Ac + LQR.kofs(kk) + r * LQR.s1;
 #pragma unroll
@@ -304,7 +306,7 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT, HX_MINB_BP3_OF(N))
 #pragma unroll
       for (int t = 0; t < m; ++t) l[t] = y[t];
       if constexpr (kSerial) asm volatile("" ::: "memory");
-      l = Bc + LQS.kofs(kk) + r;
+      l = Bc + LQS.kofs(ln_c / m) + ln_c % m;
 #pragma unroll
       for (int t = 0; t < m; ++t) x[t] = l[t * LQS.s1];
       fold_apply<m, m, -1>(p.Dt, x, y);
@@ -335,7 +337,7 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT, HX_MINB_BP3_OF(N))
     // ---- S8: i-lines (k, a): project along r
     if (el_b < ne) {
       int k, a;
-      iline_coords<n, m, C::ORD>(ln_b, k, a);
+      iline_coords<n, m, (C::ORD & 4)>(ln_b, k, a);
       const double* src = Cb + LZ.kofs(k) + a * LZ.s1;
       double x[m], y[n];
 #pragma unroll

@@ -48,6 +48,10 @@ BP3_SER = _degrees("HX_GEN_BP3_SER", {10, 12, 13})
 # N=12 0.852 -> 0.943, N=13 0.747 -> 0.791 and N=14 0.788 -> 0.823 at MINB 2,
 # N=15 0.815 -> 0.882; slower at N <= 10, where the registers are there).
 BP35_LEAN = _degrees("HX_GEN_BP35_LEAN", set(range(11, 16)))
+# BP3.0 degrees (even m) whose S4 / S6 i-line lane order may be k-fastest
+# (ORD bit 8), chosen by the model against the default (r2_26: N=4 0.84 ->
+# 0.87, N=6 0.90 -> 0.92, N=8 0.78 -> 0.79, N=10 0.70 -> 0.72)
+BP3_KI = _degrees("HX_GEN_BP3_KI", {2, 4, 6, 8, 10, 12, 14})
 # BP3.0 degrees whose layouts weight each access pattern by the number of
 # passes that use it (phases()) instead of counting every pattern once
 # (r2_16: N=10 0.687 -> 0.706, N=12 0.598 -> 0.613, equal elsewhere; at
@@ -207,7 +211,12 @@ def phases(bp, n, m, ord_=0):
     # (n, m, .) tensors (S2, S8: pattern 6).  The (m, m, m) stages S4 / S6 keep
     # theirs: with odd m the unpaired last slice costs more than it saves
     # (r11: 1.3-1.5x wavefronts there with pattern 6 / 7).
-    pi = 6 if ord_ == 4 else 2
+    # ORD bit 8: the i-line halves of S4 / S6 (over the (m, m, m) tensors T
+    # and QR) enumerate their lines k-fastest (pattern 5): with even m an
+    # even row stride confines i-line starts to every other bank pair, and
+    # k-fastest lanes spread them again (model: N=8 1.28x -> 1.16x).
+    pi = 6 if ord_ & 4 else 2
+    pm = 5 if ord_ & 8 else 2
     if n - 1 in BP3_WEIGHTED:
         # patterns weighted by the passes each tensor sees (hx_bp3.cu): X is
         # written in S1 and S8, read in S2 and S9; QR / QS are read and
@@ -216,12 +225,12 @@ def phases(bp, n, m, ord_=0):
         # ways and by S5 (with ACCS also re-read, rewritten twice and read
         # by S7 -- ACCS degrees are searched jointly with Z, see plan())
         wt = 7 if n - 1 in BP3_ACCS else 2
-        return [(0, (n, m, n), ((1, 2), (pi, 2))), (0, (m, m, m), ((0, 3), (2, 3))),
+        return [(0, (n, m, n), ((1, 2), (pi, 2))), (0, (m, m, m), ((0, 3), (pm, 3))),
                 (1, (n, m, m), ((0, 1), (pi, 1))), (1, (m, m, m), ((0, 3), (1, 3))),
-                (2, (m, m, m), ((0, wt), (1, 1), (2, 1))), (2, (n, m, m), ((0, 1), (pi, 1)))]
-    return [(0, (n, m, n), (1, pi)), (0, (m, m, m), (0, 2)),
+                (2, (m, m, m), ((0, wt), (1, 1), (pm, 1))), (2, (n, m, m), ((0, 1), (pi, 1)))]
+    return [(0, (n, m, n), (1, pi)), (0, (m, m, m), (0, pm)),
             (1, (n, m, m), (0, pi)), (1, (m, m, m), (0, 1)),
-            (2, (m, m, m), (0, 1, 2)), (2, (n, m, m), (0, pi))]
+            (2, (m, m, m), (0, 1, pm)), (2, (n, m, m), (0, pi))]
 
 
 def q_stage_stride(n):
@@ -254,6 +263,8 @@ def plan(bp, deg, target=TARGET_THREADS, qstage=False):
     # fewer conflicts (r11/r12: latency-bound, not shared-memory-bound), so
     # the search stays on the default order there
     ords = {BP1: (0, 2, 4), INTERP: (0, 2, 4)}.get(bp, (0,))
+    if bp == BP3 and m % 2 == 0 and deg in BP3_KI:
+        ords = (0, 8)
     best = None
     for o in ords:  # BP1.0: lane orders chosen jointly with the strides
         ph_o = phases(bp, n, m, o)
