@@ -73,10 +73,10 @@ __global__ void __launch_bounds__(kBaseThreads)
 
 // t[e][p] *= GwJ[e][p]  (operators.py:277); BP1.0's packed GwJ slot, which is
 // i-major (hx_bp1.cu S3): point p = (k, j, i) of the (m, m, m) tensor at
-// i*m^2 + k*m + j
+// bp1_gwj_index(k, j, i, m, cfast)
 __global__ void __launch_bounds__(kBaseThreads)
     scale_kernel(double* __restrict__ t, const double* __restrict__ fac, int64_t n_el, int m,
-                 int64_t estride, int* flag) {
+                 int64_t estride, int cfast, int* flag) {
   const int P = m * m * m;
   const int64_t total = n_el * P;
   for (int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; g < total;
@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(kBaseThreads)
     const int k = p / (m * m), j = (p / m) % m, i = p % m;
     const double v = t[g];
     if (flag && nonfinite(v)) atomicOr(flag, 1);  // non-finite q propagates into I q
-    t[g] = fac[e * estride + (i * m + k) * m + j] * v;
+    t[g] = fac[e * estride + bp1_gwj_index(k, j, i, m, cfast)] * v;
   }
 }
 
@@ -189,6 +189,7 @@ static cudaError_t baseline_n(const hx_plan& P, const double* q, const double* f
   if (P.bp == HX_BP1) {
     HX_TRY((interp3<n, m>(P.interp, q, w0, w1, w2, E, s)));
     scale_kernel<<<base_blocks(E * m3), kBaseThreads, 0, s>>>(w2, fac, E, m, P.elem_stride,
+                                                              int(bp1_gwj_cfast(P.degree)),
                                                               flag);
     HX_TRY(cudaGetLastError());
     return project3<n, m>(P.interp, w2, w0, w1, out, E, s);

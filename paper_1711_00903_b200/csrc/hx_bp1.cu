@@ -64,6 +64,7 @@ struct BP1Params {
   Fold<N + 1, N + 2> It;  // its transpose (projection)
   const double* q;
   const double* gwj;  // packed, i-major per element: gwj[e * fac_estride + a * m^2 + c * m + b]
+                      // (+ b * m + c with ORD bit 8: bp1_gwj_index)
   double* out;
   int64_t n_el;
   int64_t fac_estride;
@@ -79,7 +80,10 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT, HX_MINB_BP1_OF(N))
   constexpr int EPB = C::EPB, NT = C::NT;
   constexpr Lay LX = C::L[0], LY = C::L[1];
   constexpr int EX = C::EBUF[0], EY = C::EBUF[1];
-  constexpr int JORD = C::ORD;  // lane order of the j-line stages S2, S4
+  constexpr int JORD = C::ORD & 7;  // lane order of the j-line stages S2, S4
+  // ORD bit 8: S3's lines run c-fastest, and the packed GwJ slot is stored
+  // (i, j, k) -- gwj[a][b][c] -- so the S3 loads stay one contiguous run
+  constexpr bool kCFast = (C::ORD & 8) != 0;
   // a thread owns one line per stage when NT covers the tile's lines, else
   // it walks over several (small CTAs: cheap barriers, many CTAs per SM)
   constexpr bool ONE_C = EPB * m2 <= NT;
@@ -167,7 +171,7 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT, HX_MINB_BP1_OF(N))
     for_lines<EPB * m2, NT>(tid, [&](int g) {
       const int el = g / m2, ln = g % m2;
       if (el >= ne) return;
-      const int c = ln / m, b = ln % m;
+      const int c = kCFast ? ln % m : ln / m, b = kCFast ? ln / m : ln % m;
       double wl[m];
       if constexpr (ONE_C) {
 #pragma unroll
@@ -267,6 +271,19 @@ static cudaError_t launch_n(const hx_plan& P, const double* q, const double* fac
   prm.flag = flag;
   prm.energy = energy;
   return energy ? launch_t<N, true>(prm, n_el, s) : launch_t<N, false>(prm, n_el, s);
+}
+
+bool bp1_gwj_cfast(int degree) {
+  switch (degree) {
+#define HX_CASE(N) \
+  case N:          \
+    return (Cfg<kBP1, N>::ORD & 8) != 0;
+    HX_CASE(1) HX_CASE(2) HX_CASE(3) HX_CASE(4) HX_CASE(5) HX_CASE(6) HX_CASE(7) HX_CASE(8)
+    HX_CASE(9) HX_CASE(10) HX_CASE(11) HX_CASE(12) HX_CASE(13) HX_CASE(14) HX_CASE(15)
+#undef HX_CASE
+    default:
+      return false;
+  }
 }
 
 cudaError_t launch_bp1(const hx_plan& P, const double* q, const double* fac, double* out,

@@ -14,6 +14,7 @@ struct GeomParams {
   int64_t estride, sstride;
   int q;         // points per axis
   int gwj_only;  // 1: write only GwJ into slot 0
+  int gwj_cfast; // BP1.0 GwJ slot order (bp1_gwj_index)
   int* flag;
 };
 
@@ -60,8 +61,8 @@ __global__ void geometry_kernel(const __grid_constant__ GeomParams p) {
   if (!(det > 1e-14) && p.flag) atomicOr(p.flag, 2);
   const double w3 = p.weights[ii] * p.weights[jj] * p.weights[kk];
   if (p.gwj_only) {
-    // BP1.0's packed slot is i-major (hx_bp1.cu S3): point (k, j, i) at i*q^2 + k*q + j
-    p.fac[e * p.estride + (ii * q + kk) * q + jj] = w3 * det;
+    // BP1.0's packed slot is i-major (hx_bp1.cu S3): bp1_gwj_index
+    p.fac[e * p.estride + bp1_gwj_index(kk, jj, ii, q, p.gwj_cfast)] = w3 * det;
     return;
   }
   double* dst = p.fac + e * p.estride + pt;
@@ -93,6 +94,7 @@ cudaError_t launch_geometry(const hx_plan& P, const double* verts, int64_t n_el,
   g.sstride = P.slot_stride;
   const bool gwj_only = !all_slots && P.n_slots == 1;
   g.gwj_only = gwj_only;
+  g.gwj_cfast = gwj_only && bp1_gwj_cfast(P.degree);
   g.estride = all_slots ? 7 * P.slot_stride : P.elem_stride;
   g.flag = flag;
   const int64_t total = n_el * int64_t(P.q) * P.q * P.q;
@@ -113,11 +115,12 @@ __global__ void repack_kernel(const double* __restrict__ src, double* __restrict
   const int rem = int(gid % per);
   const int sl = rem / q3, pt = rem % q3;
   const int64_t ref = (e * 7 + first_slot + sl) * q3 + pt;
-  // BP1.0's single packed slot is i-major (hx_bp1.cu S3): (k, j, i) at i*q^2 + k*q + j
+  // BP1.0's single packed slot is i-major (hx_bp1.cu S3): bp1_gwj_index,
+  // imajor = 1 + cfast
   int ppt = pt;
   if (imajor) {
     const int kk = pt / (q * q), jj = (pt / q) % q, ii = pt % q;
-    ppt = (ii * q + kk) * q + jj;
+    ppt = bp1_gwj_index(kk, jj, ii, q, imajor == 2);
   }
   const int64_t pk = (e * nslot + sl) * sstride + ppt;
   if (to_packed)
@@ -135,7 +138,7 @@ cudaError_t launch_repack(const hx_plan& P, const double* src, int64_t n_el, dou
   const int first = (to_packed && P.n_slots == 1) ? 6 : 0;
   const int64_t total = n_el * int64_t(nslot) * q3;
   const int threads = 256;
-  const int imajor = to_packed && P.n_slots == 1;
+  const int imajor = (to_packed && P.n_slots == 1) ? 1 + int(bp1_gwj_cfast(P.degree)) : 0;
   repack_kernel<<<unsigned((total + threads - 1) / threads), threads, 0, s>>>(
       src, dst, n_el, P.q, nslot, first, P.slot_stride, to_packed, imajor);
   return cudaGetLastError();

@@ -59,6 +59,14 @@ std::vector<int64_t> chunk_schedule(int64_t n_el, int64_t chunk_el);
 cudaError_t pipe_setup(hx_plan* P);
 int cuda_status(cudaError_t err);
 
+// BP1.0's packed GwJ slot order for a degree: point (k, j, i) of the
+// (m, m, m) GL tensor lives at i*m^2 + k*m + j, or -- when the degree's S3
+// runs c-fastest (Cfg ORD bit 8, hx_bp1.cu) -- at i*m^2 + j*m + k
+bool bp1_gwj_cfast(int degree);
+__host__ __device__ inline int bp1_gwj_index(int k, int j, int i, int m, bool cfast) {
+  return cfast ? (i * m + j) * m + k : (i * m + k) * m + j;
+}
+
 // launch the fused element kernel for elements [0, n_el) of device arrays
 cudaError_t launch_bp1(const hx_plan& P, const double* q, const double* fac, double* out,
                        int64_t n_el, int* flag, double* energy, cudaStream_t s);

@@ -48,6 +48,10 @@ BP3_SER = _degrees("HX_GEN_BP3_SER", {10, 12, 13})
 # N=12 0.852 -> 0.943, N=13 0.747 -> 0.791 and N=14 0.788 -> 0.823 at MINB 2,
 # N=15 0.815 -> 0.882; slower at N <= 10, where the registers are there).
 BP35_LEAN = _degrees("HX_GEN_BP35_LEAN", set(range(11, 16)))
+# BP1.0 degrees whose S3 lane order may be c-fastest with the GwJ slot
+# stored (i, j, k) (ORD bit 8; hx_bp1.cu, hx_geom.cu), chosen by the model
+# (picked at N = 4, 8, 10, 12; r2_28: N=4 0.79 -> 0.82, N=12 0.51 -> 0.52)
+BP1_CFAST = _degrees("HX_GEN_BP1_CFAST", {2, 4, 6, 8, 10, 12, 14})
 # BP3.0 degrees (even m) whose S4 / S6 i-line lane order may be k-fastest
 # (ORD bit 8), chosen by the model against the default (r2_26: N=4 0.84 ->
 # 0.87, N=6 0.90 -> 0.92, N=8 0.78 -> 0.79, N=10 0.70 -> 0.72)
@@ -198,8 +202,12 @@ def phases(bp, n, m, ord_=0):
         # line L is congruent to a multiple of L mod 16 in every stage when
         # X = (73, 8) and Y = (153, 17) at N=7 (ncu r2_03: the i-fastest /
         # c-paired orders left 1.7x wavefronts in S3 or in S2 / S4).
-        pj = {0: 1, 2: 4, 4: 7}[ord_]
-        return [(0, (m, n, n), (0, pj)), (1, (m, m, n), (pj, 2))]
+        # ORD bit 8 (BP1_CFAST degrees): S3's lanes run c-fastest (pattern 5)
+        # and the packed GwJ slot is stored (i, j, k) so its loads stay
+        # contiguous -- with even m an even Y row stride otherwise leaves
+        # the i-line starts on every other bank pair (model N=8: 1.71x).
+        pj = {0: 1, 2: 4, 4: 7}[ord_ & 7]
+        return [(0, (m, n, n), (0, pj)), (1, (m, m, n), (pj, 5 if ord_ & 8 else 2))]
     if bp == INTERP:
         # ORD: lane order of the i-line stages (S2, S4): 0 a fastest (pattern
         # 2), 2 k fastest (5), 4 k-paired (6, with k-paired layouts).  The
@@ -265,6 +273,8 @@ def plan(bp, deg, target=TARGET_THREADS, qstage=False):
     ords = {BP1: (0, 2, 4), INTERP: (0, 2, 4)}.get(bp, (0,))
     if bp == BP3 and m % 2 == 0 and deg in BP3_KI:
         ords = (0, 8)
+    if bp == BP1 and deg in BP1_CFAST:
+        ords = ords + tuple(o | 8 for o in ords)
     best = None
     for o in ords:  # BP1.0: lane orders chosen jointly with the strides
         ph_o = phases(bp, n, m, o)
