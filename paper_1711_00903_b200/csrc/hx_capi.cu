@@ -316,6 +316,7 @@ cudaError_t pipe_setup(hx_plan* P) {
   // nothing recorded yet: waiting on it is a no-op
   P->pipe_dev = dev;
   P->pipe_ready = true;
+  P->pipe_cont = false;  // fresh slot events: the next overlapped call starts a new sequence
   return cudaSuccess;
 }
 
