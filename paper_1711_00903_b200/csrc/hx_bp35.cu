@@ -223,7 +223,9 @@ __global__ void __launch_bounds__(Cfg<kBP35, N>::NT, HX_MINB_BP35_OF(N))
         st_stream(dst + k * n2, (kLean ? a[k * LA.s0] : acc[k]) + b[k * LB.s0] + c[k * LC.s0]);
     }
     // A is rewritten by the next tile's S1 only after it has passed this
-    // tile's S3/S4 barriers; B and C only after the next S1 barrier.
+    // tile's S3/S4 barriers (with kLean, S5 reads only the thread's own
+    // k-line of A, which the same thread rewrites in the next S1); B and C
+    // only after the next S1 barrier.
   }
   if constexpr (ENERGY) {
     const double sum = block_sum<C::NT>(en, A);  // A is idle after the last S3
