@@ -106,6 +106,10 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT, HX_MINB_BP3_OF(N))
     prefetch_l2(p.q + HX_QEL(e0) * n3, ne * n3 * sizeof(double));
   }
 
+  // PDL (hx_common.cuh): only L2 prefetch hints above this point
+  pdl_allow_dependents();
+  pdl_wait();
+
   const int el_a = tid / n2, ln_a = tid % n2;
   const int el_b = tid / (n * m), ln_b = tid % (n * m);
   const int el_c = tid / m2, ln_c = tid % m2;
@@ -374,20 +378,19 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT, HX_MINB_BP3_OF(N))
 }
 
 template <int N, bool E, class Prm>
-static cudaError_t launch_t(const Prm& prm, int64_t n_el, cudaStream_t s) {
+static cudaError_t launch_t(const Prm& prm, int64_t n_el, cudaStream_t s, bool pdl) {
   using C = Cfg<kBP3, N>;
   constexpr int smem = smem_doubles<kBP3, N>() * int(sizeof(double));
   const int64_t ntiles = (n_el + C::EPB - 1) / C::EPB;
   unsigned grid = 0;
   const cudaError_t err = persistent_grid<bp3_kernel<N, E>>(C::NT, smem, ntiles, &grid);
   if (err != cudaSuccess) return err;
-  bp3_kernel<N, E><<<grid, C::NT, smem, s>>>(prm);
-  return cudaGetLastError();
+  return launch_kernel<bp3_kernel<N, E>>(grid, C::NT, smem, s, pdl, prm);
 }
 
 template <int N>
 static cudaError_t launch_n(const hx_plan& P, const double* q, const double* fac, double* out,
-                            int64_t n_el, int* flag, double* energy, cudaStream_t s) {
+                            int64_t n_el, int* flag, double* energy, cudaStream_t s, bool pdl) {
   using C = Cfg<kBP3, N>;
   constexpr int n = N + 1, m = N + 2;
   constexpr int smem = smem_doubles<kBP3, N>() * int(sizeof(double));
@@ -408,15 +411,15 @@ static cudaError_t launch_n(const hx_plan& P, const double* q, const double* fac
   prm.lam = P.lam;
   prm.flag = flag;
   prm.energy = energy;
-  return energy ? launch_t<N, true>(prm, n_el, s) : launch_t<N, false>(prm, n_el, s);
+  return energy ? launch_t<N, true>(prm, n_el, s, pdl) : launch_t<N, false>(prm, n_el, s, pdl);
 }
 
 cudaError_t launch_bp3(const hx_plan& P, const double* q, const double* fac, double* out,
-                       int64_t n_el, int* flag, double* energy, cudaStream_t s) {
+                       int64_t n_el, int* flag, double* energy, cudaStream_t s, bool pdl) {
   switch (P.degree) {
 #define HX_CASE(N) \
   case N:          \
-    return launch_n<N>(P, q, fac, out, n_el, flag, energy, s);
+    return launch_n<N>(P, q, fac, out, n_el, flag, energy, s, pdl);
     HX_CASE(1) HX_CASE(2) HX_CASE(3) HX_CASE(4) HX_CASE(5) HX_CASE(6) HX_CASE(7) HX_CASE(8)
     HX_CASE(9) HX_CASE(10) HX_CASE(11) HX_CASE(12) HX_CASE(13) HX_CASE(14) HX_CASE(15)
 #undef HX_CASE

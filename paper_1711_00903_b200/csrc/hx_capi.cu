@@ -49,15 +49,15 @@ static int kernel_shape(int bp, int degree, int* epb, int* nt, int* smem) {
 }
 
 cudaError_t launch_apply(const hx_plan& P, const double* q, const double* fac, double* out,
-                         int64_t n_el, int* flag, cudaStream_t s, double* energy) {
+                         int64_t n_el, int* flag, cudaStream_t s, double* energy, bool pdl) {
   if (n_el == 0) return cudaSuccess;
   switch (P.bp) {
     case HX_BP1:
-      return launch_bp1(P, q, fac, out, n_el, flag, energy, s);
+      return launch_bp1(P, q, fac, out, n_el, flag, energy, s, pdl);
     case HX_BP35:
-      return launch_bp35(P, q, fac, out, n_el, flag, energy, s);
+      return launch_bp35(P, q, fac, out, n_el, flag, energy, s, pdl);
     default:
-      return launch_bp3(P, q, fac, out, n_el, flag, energy, s);
+      return launch_bp3(P, q, fac, out, n_el, flag, energy, s, pdl);
   }
 }
 
@@ -92,6 +92,13 @@ int cuda_status(cudaError_t err) {
 using namespace hx;
 
 namespace hx {
+// Device-path applies (hx_apply, hx_apply_range, hx_apply_energy) launch as
+// programmatic dependent launches (hx_common.cuh): back-to-back applies on a
+// stream overlap one kernel's retiring CTAs with the next one's start.
+#ifndef HX_APPLY_PDL
+#define HX_APPLY_PDL 1
+#endif
+constexpr bool kApplyPdl = HX_APPLY_PDL != 0;
 // NVTX range names per operator ("hx_apply BP1.0", ...)
 static const char* range_name(const hx_plan& P, const char* what) {
   static const char* names[3][4] = {
@@ -199,7 +206,8 @@ int hx_apply(const hx_plan* P, const double* q, const double* factors, double* o
        reinterpret_cast<uintptr_t>(out)) & 7)
     return HX_EINVAL;
   hx::NvtxRange range(hx::range_name(*P, "apply"));
-  return cuda_status(launch_apply(*P, q, factors, out, n_el, flag, static_cast<cudaStream_t>(stream)));
+  return cuda_status(launch_apply(*P, q, factors, out, n_el, flag, static_cast<cudaStream_t>(stream),
+                                  nullptr, kApplyPdl));
 }
 
 int hx_apply_range(const hx_plan* P, const double* q, const double* factors, double* out,
@@ -437,7 +445,7 @@ int hx_apply_energy(const hx_plan* P, const double* q, const double* factors, do
   hx::NvtxRange range(hx::range_name(*P, "energy"));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   cudaError_t err = cudaMemsetAsync(partials, 0, sizeof(double) * n_partials, s);
-  if (err == cudaSuccess) err = launch_apply(*P, q, factors, out, n_el, flag, s, partials);
+  if (err == cudaSuccess) err = launch_apply(*P, q, factors, out, n_el, flag, s, partials, kApplyPdl);
   if (err == cudaSuccess) err = launch_sum(partials, int(n_partials), energy, s);
   return cuda_status(err);
 }

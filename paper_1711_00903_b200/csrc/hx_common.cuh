@@ -215,6 +215,35 @@ inline cudaError_t resident_blocks(int threads, int smem, int* blocks) {
   return cudaSuccess;
 }
 
+// Programmatic dependent launch (PDL).  A persistent element kernel launched
+// with cudaLaunchAttributeProgrammaticStreamSerialization may start while
+// the previous kernel of the stream is still retiring its last CTAs: it only
+// issues L2 prefetch hints before pdl_wait(), which returns once the
+// previous grid has completed and its memory is visible, so every load of
+// q / factors and every store of out keeps plain stream order.
+// pdl_allow_dependents() lets the next such launch do the same with ours.
+// Both are no-ops for a plain launch.
+__device__ __forceinline__ void pdl_allow_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <auto K, class Prm>
+inline cudaError_t launch_kernel(unsigned grid, int threads, int smem, cudaStream_t s, bool pdl,
+                                 const Prm& prm) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = size_t(smem);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, K, prm);
+}
+
 // Persistent grid for `ntiles` tiles of kernel K on the current device.
 template <auto K>
 inline cudaError_t persistent_grid(int threads, int smem, int64_t ntiles, unsigned* grid) {

@@ -167,6 +167,35 @@ def test_adjoint_symmetry_and_psd(bp, deg, perturbed_single, rng):
     assert np.min(np.einsum("pi,pi->p", au, us)) >= -1e-10
 
 
+def test_back_to_back_applies_on_one_stream_bitwise(mesh3):
+    """Device applies launch as programmatic dependent launches: a chain
+    x_{k+1} = A_k x_k queued on one stream with no sync -- across operators,
+    with a torch kernel rewriting the input in between -- must equal the
+    same chain run one synchronised apply at a time, bit for bit (each
+    kernel waits for its predecessor before touching q / out)."""
+    ops = [hx.make_operator(bp, 7, mesh3, lam=1.0) for bp in BPS]
+    x0 = torch.from_numpy(np.random.default_rng(9).standard_normal(
+        (mesh3.n_el, ops[0].n_p))).cuda()
+
+    def chain(sync):
+        xs, x = [], x0
+        for k in range(9):
+            op = ops[k % 3]
+            y = torch.empty_like(x)
+            hx.apply_device(op, x, y)
+            if k % 4 == 1:
+                y.mul_(0.5)  # a foreign kernel between two applies
+            if sync:
+                torch.cuda.synchronize()
+            xs.append(y)
+            x = y
+        torch.cuda.synchronize()
+        return [t.cpu().numpy() for t in xs]
+
+    for got, want in zip(chain(False), chain(True)):
+        np.testing.assert_array_equal(got, want)
+
+
 def test_element_permutation_bitwise(perturbed_mesh2, rng):
     """test_operators.py:208-220."""
     perm = rng.permutation(8)

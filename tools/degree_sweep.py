@@ -30,6 +30,9 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--timing", choices=["b2b", "per_launch"], default="b2b",
+                    help="b2b: applies back to back between one event pair (bench.py's "
+                         "headline protocol); per_launch: an event pair per launch")
     args = ap.parse_args()
     lo, hi = (int(x) for x in args.degrees.split("..")) if ".." in args.degrees \
         else (int(args.degrees),) * 2
@@ -54,15 +57,30 @@ def main():
             for _ in range(args.warmup):
                 hx.apply_device(op, q, out)
             torch.cuda.synchronize()
-            ev = []
-            for _ in range(args.steps):
-                s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                s.record()
-                hx.apply_device(op, q, out)
-                e.record()
-                ev.append((s, e))
-            torch.cuda.synchronize()
-            ms = statistics.median(s.elapsed_time(e) for s, e in ev)
+            if args.timing == "b2b":
+                # the applies back to back between one event pair (as bench.py's
+                # headline): best of three such runs
+                ms = None
+                for _ in range(3):
+                    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    torch.cuda._sleep(200_000)  # the first launch is queued before `s`
+                    s.record()
+                    for _ in range(args.steps):
+                        hx.apply_device(op, q, out)
+                    e.record()
+                    torch.cuda.synchronize()
+                    run = s.elapsed_time(e) / args.steps
+                    ms = run if ms is None else min(ms, run)
+            else:  # per-launch events (round-1 protocol)
+                ev = []
+                for _ in range(args.steps):
+                    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    s.record()
+                    hx.apply_device(op, q, out)
+                    e.record()
+                    ev.append((s, e))
+                torch.cuda.synchronize()
+                ms = statistics.median(s.elapsed_time(e) for s, e in ev)
             t = hx.traffic(bp, deg, mesh.n_el)
             nbytes = t.bytes_per_element * mesh.n_el
             rec = {"bp": bp, "degree": deg, "n_el": mesh.n_el, "dofs": mesh.n_el * op.n_p,
@@ -70,7 +88,7 @@ def main():
                    "gb_per_s": nbytes / ms / 1e6, "frac_of_measured_peak": nbytes / ms / 1e6 / peak,
                    "gflop_per_s": hx.flop_model(bp, "fused", deg) * mesh.n_el / ms / 1e6,
                    "threads": op.plan.threads, "elements_per_tile": op.plan.elements_per_tile,
-                   "smem_bytes": op.plan.smem_bytes,
+                   "smem_bytes": op.plan.smem_bytes, "timing": args.timing,
                    "lib": os.path.basename(os.environ.get("HX_LIB_PATH", "default"))}
             line = json.dumps(rec)
             print(line, flush=True)
