@@ -104,6 +104,13 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT, HX_MINB_BP1_OF(N))
     const int64_t ne = min64(EPB, p.n_el - e0);
     prefetch_l2(p.q + HX_QEL(e0) * n3, ne * n3 * sizeof(double));
     prefetch_l2(p.gwj + HX_WEL(e0) * fs, ne * fs * sizeof(double));
+    // ... and the second tile's: with back-to-back (PDL) launches this runs
+    // under the previous apply's tail (r2_40: +0.4 % at E=32768)
+    const int64_t e1 = e0 + int64_t(gridDim.x) * EPB;
+    if (e1 < p.n_el) {
+      prefetch_l2(p.q + HX_QEL(e1) * n3, min64(EPB, p.n_el - e1) * n3 * sizeof(double));
+      prefetch_l2(p.gwj + HX_WEL(e1) * fs, min64(EPB, p.n_el - e1) * fs * sizeof(double));
+    }
   }
 
   // PDL (hx_common.cuh): only L2 prefetch hints above this point
