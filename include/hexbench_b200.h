@@ -87,7 +87,12 @@ int hx_repack_factors(const hx_plan* plan, const double* src, int64_t n_el, doub
  * (operators.py:306-349) on device-resident data: out = A q for elements
  * [0, n_el).  One fused kernel launch; no allocation, no synchronisation.
  * status_flag (device int, may be NULL) receives HX_FLAG_NONFINITE if any q
- * entry is inf/nan (the reference's np.isfinite scan, fused into the load). */
+ * entry is inf/nan (the reference's np.isfinite scan, fused into the load).
+ * The kernel is a programmatic dependent launch: it may start while the
+ * previous kernel on `stream` retires, but issues nothing except L2 prefetch
+ * hints before that kernel has completed -- plain stream order for every
+ * read of q / factors and write of out (hx_apply_range and hx_apply_energy
+ * likewise).                                                                */
 int hx_apply(const hx_plan* plan, const double* q, const double* factors, double* out,
              int64_t n_el, int* status_flag, void* stream);
 
