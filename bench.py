@@ -621,43 +621,58 @@ def pcie_bandwidth(nbytes, trials=5):
             "bidirectional_ms": t_both * 1e3}
 
 
+# CG vector passes per iteration beyond the matvec's Table-1 bytes: the
+# direction update fused into the matvec's load adds r read + p write (the
+# p read is the matvec's q read); the update reads x, p, r, Ap, writes x, r
+CG_VECTOR_PASSES = 8
+CG_VECTOR_PASSES_UNFUSED = 9  # + hx_cg_direction's own p read (p rw, r read)
+
+
 def cg_report(op, mesh, iters=20, warmup=3):
-    """CG iteration throughput (paper_1711_00903_b200/cg.py): fused matvec +
-    <p,Ap>, update, direction -- 3 kernels per iteration plus 2 tiny reduces,
-    no host synchronisation.  HBM traffic per iteration = the matvec's Table-1
-    bytes + 9 vector passes (x, p, r, Ap reads/writes)."""
+    """CG iteration throughput (paper_1711_00903_b200/cg.py): the direction
+    update fused into the matvec + <p,Ap> (hx_apply_energy_dir), the update --
+    2 kernels per iteration plus 2 tiny reduces, no host synchronisation.
+    HBM traffic per iteration = the matvec's Table-1 bytes + 8 vector passes;
+    the unfused form (separate hx_cg_direction pass) is timed beside it."""
     import torch
     import paper_1711_00903_b200 as hx
     from paper_1711_00903_b200.cg import CGWorkspace, cg_iterations
 
     b = torch.randn(op.n_el, op.n_p, dtype=torch.float64, device="cuda")
     w = CGWorkspace(b)
-    cg_iterations(op, b, warmup, w)
-    torch.cuda.synchronize()
-    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s.record()
-    cg_iterations(op, b, iters, w)
-    e.record()
-    e.synchronize()
-    # subtract the per-call setup (two copies + one dot) measured separately
-    s0, e0 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s0.record()
-    cg_iterations(op, b, 0, w)
-    e0.record()
-    e0.synchronize()
-    ms = (s.elapsed_time(e) - s0.elapsed_time(e0)) / iters
-    per_el = hx.traffic(op.bp, op.degree).bytes_per_element + 9 * 8 * op.n_p
+
+    def timed(k, fused):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        cg_iterations(op, b, k, w, fuse_direction=fused)
+        e.record()
+        e.synchronize()
+        return s.elapsed_time(e)
+
+    res = {}
+    for fused in (True, False):
+        timed(warmup, fused)
+        # subtract the per-call setup (copies + one dot) measured separately
+        res[fused] = (timed(iters, fused) - timed(0, fused)) / iters
+    ms = res[True]
+    mv = hx.traffic(op.bp, op.degree).bytes_per_element
+    per_el = mv + CG_VECTOR_PASSES * 8 * op.n_p
     gbs = per_el * op.n_el / (ms * 1e-3) / 1e9
+    unf = mv + CG_VECTOR_PASSES_UNFUSED * 8 * op.n_p
     return {"bp": op.bp, "degree": op.degree, "n_el": op.n_el, "ms_per_iteration": ms,
             "gdof_iterations_per_s": op.n_el * op.n_p / (ms * 1e-3) / 1e9,
             "hbm_bytes_per_iteration": per_el * op.n_el, "achieved_gb_per_s": gbs,
-            "kernels_per_iteration": 5}
+            "kernels_per_iteration": 4,
+            "unfused_direction": {"ms_per_iteration": res[False],
+                                  "hbm_bytes_per_iteration": unf * op.n_el,
+                                  "achieved_gb_per_s": unf * op.n_el / (res[False] * 1e-3) / 1e9,
+                                  "kernels_per_iteration": 5}}
 
 
 def cg_assembled_report(side=32, iters=20, warmup=3):
     """Assembled CG (cg.cg_solve_assembled: Poisson, BP3.5 N=7 on the
-    unperturbed side^3 cube mesh, Dirichlet mask): fused matvec + <p,Ap>, the
-    update with the gather-scatter of A p fused in, direction.  Same 9 vector
+    unperturbed side^3 cube mesh, Dirichlet mask): direction update fused into
+    the matvec + <p,Ap>, the gather-scatter of A p, the update.  Same 8 vector
     passes per iteration as the element-local CG; the DSS gathers re-read
     shared-node neighbours (L2 hits)."""
     import torch
@@ -679,7 +694,7 @@ def cg_assembled_report(side=32, iters=20, warmup=3):
 
     timed(warmup)
     ms = (timed(iters) - timed(0)) / iters
-    per_el = hx.traffic(op.bp, op.degree).bytes_per_element + 9 * 8 * op.n_p
+    per_el = hx.traffic(op.bp, op.degree).bytes_per_element + CG_VECTOR_PASSES * 8 * op.n_p
     unique = (side * DEGREE + 1) ** 3
     small = small_mesh_cg_graph()
     return {"bp": op.bp, "degree": op.degree, "n_el": op.n_el, "side": side,
@@ -688,12 +703,12 @@ def cg_assembled_report(side=32, iters=20, warmup=3):
             "global_gdof_iterations_per_s": unique / (ms * 1e-3) / 1e9,
             "hbm_bytes_per_iteration": per_el * op.n_el,
             "achieved_gb_per_s": per_el * op.n_el / (ms * 1e-3) / 1e9,
-            "kernels_per_iteration": 5, "small_mesh_cuda_graph": small}
+            "kernels_per_iteration": 7, "small_mesh_cuda_graph": small}
 
 
 def small_mesh_cg_graph(side=8, iters=200):
     """Launch-bound regime: assembled CG on a side-8 cube (512 elements, N=7),
-    eager (~7 launches per iteration from Python) vs the iteration blocks
+    eager (~8 launches per iteration from Python) vs the iteration blocks
     captured once as a CUDA graph (AssembledCG(graph=True)).  Wall
     clock per iteration, including the host reads of the residual every 10
     iterations."""

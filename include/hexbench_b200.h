@@ -197,6 +197,17 @@ int hx_apply_energy(const hx_plan* plan, const double* q, const double* factors,
                     int64_t n_el, double* partials, int64_t n_partials, double* energy,
                     int* status_flag, void* stream);
 
+/* CG direction update fused into the next matvec: p = r + (*rr_new / *rr_old) p
+ * (hx_cg_direction's formula, bit for bit), then hx_apply_energy of the new p
+ * -- out = A p, *energy = <p, A p> -- in one kernel that reads p_old and r
+ * where it would read q and stores p back, so the direction update needs no
+ * pass of its own.  p, r and out must be distinct element-local arrays of
+ * n_el * (N+1)^3 doubles.  New: serves the CG driver.       */
+int hx_apply_energy_dir(const hx_plan* plan, double* p, const double* r, const double* rr_new,
+                        const double* rr_old, const double* factors, double* out, int64_t n_el,
+                        double* partials, int64_t n_partials, double* energy, int* status_flag,
+                        void* stream);
+
 /* CG vector kernels on device arrays of n doubles; scalars are device
  * pointers so an iteration never synchronises with the host.
  *   hx_dot:          *result = <u, v>

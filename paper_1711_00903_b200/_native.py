@@ -50,6 +50,8 @@ SIGNATURES = {
     "hx_interp_elements": (_c.c_int, [_c.c_int, _P, _c.c_int, _P, _P, _c.c_int64, _P, _P]),
     "hx_energy_partials": (_c.c_int64, []),
     "hx_apply_energy": (_c.c_int, [_P, _P, _P, _P, _c.c_int64, _P, _c.c_int64, _P, _P, _P]),
+    "hx_apply_energy_dir": (_c.c_int, [_P, _P, _P, _P, _P, _P, _P, _c.c_int64, _P, _c.c_int64,
+                                       _P, _P, _P]),
     "hx_dot": (_c.c_int, [_P, _P, _c.c_int64, _P, _c.c_int64, _P, _P]),
     "hx_cg_update": (_c.c_int, [_P, _P, _P, _P, _c.c_int64, _P, _P, _P, _c.c_int64, _P, _P]),
     "hx_cg_direction": (_c.c_int, [_P, _P, _c.c_int64, _P, _P, _P]),

@@ -5,9 +5,14 @@ module is new and exercises the multi-GPU dot-product path.
 
 Per iteration, all on the device and without a host synchronisation:
 
-  1. Ap = A p and <p, A p>      one fused kernel (hx_apply_energy)
+  1. beta, p = r + beta p,      one fused kernel (hx_apply_energy_dir): the
+     Ap = A p and <p, A p>      direction update rides the matvec's first load
   2. alpha, x, r, <r, r>        hx_cg_update
-  3. beta, p                    hx_cg_direction
+
+Every iteration has the same form: the solve starts from p = 0 with the
+previous <r, r> slot set to 1, so the first direction is p = r + rr * 0 = r
+exactly.  ``fuse_direction=False`` runs step 1 as hx_cg_direction followed
+by hx_apply_energy -- the same arithmetic, bit for bit (tests/test_gpu_cg.py).
 
 Under torch.distributed each rank owns a contiguous element range
 (shard.partition) and the two scalars are all-reduced (8 bytes each, NCCL)
@@ -47,6 +52,22 @@ def _allreduce(t, group):
             dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
 
 
+def _direction_apply(op, w, ap, cur, flag, strm, fused):
+    """Step 1: p = r + (rr[cur] / rr[1 - cur]) p, then ap = A p, pap = <p, A p>."""
+    L, ptr = _native.lib(), _native.ptr
+    if fused:
+        _native.check(L.hx_apply_energy_dir(op.plan.handle, ptr(w.p), ptr(w.r), ptr(w.rr[cur]),
+                                            ptr(w.rr[1 - cur]), ptr(op.device_factors), ptr(ap),
+                                            op.n_el, ptr(w.partials), w.npart, ptr(w.pap),
+                                            ptr(flag), strm), "hx_apply_energy_dir")
+        return
+    _native.check(L.hx_cg_direction(ptr(w.p), ptr(w.r), w.p.numel(), ptr(w.rr[cur]),
+                                    ptr(w.rr[1 - cur]), strm), "hx_cg_direction")
+    _native.check(L.hx_apply_energy(op.plan.handle, ptr(w.p), ptr(op.device_factors), ptr(ap),
+                                    op.n_el, ptr(w.partials), w.npart, ptr(w.pap), ptr(flag),
+                                    strm), "hx_apply_energy")
+
+
 class CGWorkspace:
     """Device scratch of one solve: vectors p, r, Ap and the scalar slots."""
 
@@ -62,9 +83,15 @@ class CGWorkspace:
         self.rr = [torch.zeros(1, dtype=torch.float64, device=like.device) for _ in range(2)]
         self.pap = torch.zeros(1, dtype=torch.float64, device=like.device)
 
+    def start(self):
+        """p = 0 and the previous <r, r> slot = 1: the first (uniform) step's
+        direction update yields p = r exactly (rr[0] must hold <r, r>)."""
+        self.p.zero_()
+        self.rr[1].fill_(1.0)
+
 
 def cg_solve(op, b, x0=None, tol=1e-10, maxiter=500, check_every=10, group=None, work=None,
-             graph=False):
+             graph=False, fuse_direction=True):
     """Solve A x = b for a device-resident right-hand side.
 
     ``op`` is an OperatorInstance (or this rank's ShardedOperator.op); ``b`` a
@@ -72,7 +99,8 @@ def cg_solve(op, b, x0=None, tol=1e-10, maxiter=500, check_every=10, group=None,
     ||r|| <= tol * ||b|| (checked every ``check_every`` iterations).
     ``graph=True`` (single process): the iterations between two checks run as
     one captured CUDA graph (see AssembledCG); same iterates bit for bit, the
-    iteration count rounded up to whole blocks.
+    iteration count rounded up to whole blocks.  ``fuse_direction``: see the
+    module docstring.
     """
     import torch
 
@@ -91,11 +119,11 @@ def cg_solve(op, b, x0=None, tol=1e-10, maxiter=500, check_every=10, group=None,
         _native.check(L.hx_apply(op.plan.handle, ptr(x), ptr(op.device_factors), ptr(w.ap),
                                  op.n_el, ptr(flag), stream), "hx_apply")
         torch.sub(b, w.ap, out=w.r)
-    w.p.copy_(w.r)
     cur = 0
     _native.check(L.hx_dot(ptr(w.r), ptr(w.r), n, ptr(w.partials), w.npart, ptr(w.rr[cur]),
                            stream), "hx_dot")
     _allreduce(w.rr[cur], group)
+    w.start()
     bb = torch.zeros(1, dtype=torch.float64, device=dev)
     _native.check(L.hx_dot(ptr(b), ptr(b), n, ptr(w.partials), w.npart, ptr(bb), stream))
     _allreduce(bb, group)
@@ -108,19 +136,13 @@ def cg_solve(op, b, x0=None, tol=1e-10, maxiter=500, check_every=10, group=None,
 
     def step(c, strm):
         nx = 1 - c
-        _native.check(L.hx_apply_energy(op.plan.handle, ptr(w.p), ptr(op.device_factors),
-                                        ptr(w.ap), op.n_el, ptr(w.partials), w.npart,
-                                        ptr(w.pap), ptr(flag), strm), "hx_apply_energy")
+        _direction_apply(op, w, w.ap, c, flag, strm, fuse_direction)
         _allreduce(w.pap, group)
         _native.check(L.hx_cg_update(ptr(x), ptr(w.p), ptr(w.r), ptr(w.ap), n, ptr(w.rr[c]),
                                      ptr(w.pap), ptr(w.partials), w.npart, ptr(w.rr[nx]),
                                      strm), "hx_cg_update")
         _allreduce(w.rr[nx], group)
         return nx
-
-    def direction(c, nx, strm):
-        _native.check(L.hx_cg_direction(ptr(w.p), ptr(w.r), n, ptr(w.rr[nx]), ptr(w.rr[c]),
-                                        strm), "hx_cg_direction")
 
     import torch.distributed as dist
     if graph and not (dist.is_available() and dist.is_initialized()):
@@ -129,9 +151,7 @@ def cg_solve(op, b, x0=None, tol=1e-10, maxiter=500, check_every=10, group=None,
         def block():
             c, strm = 0, _stream(dev)
             for _ in range(k):
-                nx = step(c, strm)
-                direction(c, nx, strm)
-                c = nx
+                c = step(c, strm)
 
         run = block  # first block eager (first-launch setup), then captured
         while it < maxiter:
@@ -152,14 +172,13 @@ def cg_solve(op, b, x0=None, tol=1e-10, maxiter=500, check_every=10, group=None,
                 if norms[-1] <= target:
                     converged = True
                     break
-            direction(cur, nxt, stream)
             cur = nxt
     if int(flag.item()) & _native.HX_FLAG_NONFINITE:
         raise ValueError("non-finite values during the CG solve")
     return CGResult(x, it, converged, norms)
 
 
-def cg_iterations(op, b, iterations, work, stream=None):
+def cg_iterations(op, b, iterations, work, stream=None, fuse_direction=True):
     """Run exactly ``iterations`` CG steps from x = 0 without convergence
     checks or host synchronisation (the harness times this)."""
     import torch
@@ -171,16 +190,14 @@ def cg_iterations(op, b, iterations, work, stream=None):
     x = torch.zeros_like(b)
     w = work
     w.r.copy_(b)
-    w.p.copy_(b)
     cur = 0
     L.hx_dot(ptr(w.r), ptr(w.r), n, ptr(w.partials), w.npart, ptr(w.rr[cur]), stream)
+    w.start()
     for _ in range(iterations):
         nxt = 1 - cur
-        L.hx_apply_energy(op.plan.handle, ptr(w.p), ptr(op.device_factors), ptr(w.ap),
-                          op.n_el, ptr(w.partials), w.npart, ptr(w.pap), None, stream)
+        _direction_apply(op, w, w.ap, cur, None, stream, fuse_direction)
         L.hx_cg_update(ptr(x), ptr(w.p), ptr(w.r), ptr(w.ap), n, ptr(w.rr[cur]), ptr(w.pap),
                        ptr(w.partials), w.npart, ptr(w.rr[nxt]), stream)
-        L.hx_cg_direction(ptr(w.p), ptr(w.r), n, ptr(w.rr[nxt]), ptr(w.rr[cur]), stream)
         cur = nxt
     return x
 
@@ -309,27 +326,26 @@ class _AssembledState:
 
 
 def _assembled_setup(op, side, b, st, stream):
-    """r = mask dss(b) (b exchanged through the halo buffer), p = r, <r, r>."""
+    """r = mask dss(b) (b exchanged through the halo buffer), <r, r>, p = 0
+    (CGWorkspace.start: the first step's direction update gives p = r)."""
     L, ptr, sh, w = _native.lib(), _native.ptr, st.sh, st.w
     sh.own(st.ap_pad).copy_(b)
     sh.exchange(st.ap_pad)
     gather_scatter(st.ap_pad, side, op.degree, st.mask, out=w.r, stream=stream, shard=sh)
-    w.p.copy_(w.r)
     _native.check(L.hx_dot_dss(ptr(w.r), ptr(w.r), side, op.degree, sh.lo, sh.hi,
                                ptr(w.partials), w.npart, ptr(w.rr[0]), stream), "hx_dot_dss")
     _global_sum(w.rr[0], sh)
+    w.start()
 
 
-def _assembled_step(op, side, st, cur, stream, flag=None):
-    """One CG iteration; returns the index of the new <r, r> slot.  A p is
-    assembled in place over the halo-padded buffer by the separable face
-    passes, then read by the masked update (hx_cg_update_assembled)."""
+def _assembled_step(op, side, st, cur, stream, flag=None, fused=True):
+    """One CG iteration (direction update fused into the matvec); returns the
+    index of the new <r, r> slot.  A p is assembled in place over the
+    halo-padded buffer by the separable face passes, then read by the masked
+    update (hx_cg_update_assembled)."""
     L, ptr, sh, w = _native.lib(), _native.ptr, st.sh, st.w
     nxt = 1 - cur
-    ap_own = sh.own(st.ap_pad)
-    _native.check(L.hx_apply_energy(op.plan.handle, ptr(w.p), ptr(op.device_factors),
-                                    ptr(ap_own), op.n_el, ptr(w.partials), w.npart, ptr(w.pap),
-                                    ptr(flag), stream), "hx_apply_energy")
+    _direction_apply(op, w, sh.own(st.ap_pad), cur, flag, stream, fused)
     _global_sum(w.pap, sh)
     sh.exchange(st.ap_pad)
     _native.check(L.hx_cg_update_assembled(ptr(st.x), ptr(w.p), ptr(w.r), ptr(st.ap_pad), side,
@@ -368,10 +384,11 @@ class AssembledCG:
     count is rounded up to whole blocks."""
 
     def __init__(self, op, side, mask_boundary=True, check_every=10, shard=None, graph=False,
-                 work=None):
+                 work=None, fuse_direction=True):
         import torch
 
         self.op, self.side, self.check_every = op, side, check_every
+        self.fused = fuse_direction
         self.dev = op.device
         like = torch.zeros((op.n_el, op.n_p), dtype=torch.float64, device=self.dev)
         self.st = _AssembledState(op, side, like, mask_boundary, work, shard)
@@ -387,20 +404,11 @@ class AssembledCG:
             self._block()
             self.replay = _graphed(self._block)
 
-    def _direction(self, cur, nxt, strm):
-        w = self.st.w
-        _native.check(_native.lib().hx_cg_direction(_native.ptr(w.p), _native.ptr(w.r),
-                                                    w.p.numel(), _native.ptr(w.rr[nxt]),
-                                                    _native.ptr(w.rr[cur]), strm),
-                      "hx_cg_direction")
-
     def _block(self):
         c = 0
         strm = _stream(self.dev)
         for _ in range(self.k):
-            nx = _assembled_step(self.op, self.side, self.st, c, strm, self.flag)
-            self._direction(c, nx, strm)
-            c = nx
+            c = _assembled_step(self.op, self.side, self.st, c, strm, self.flag, self.fused)
 
     def solve(self, b, tol=1e-10, maxiter=1000):
         """Solve for the (rank's) element-local load vector ``b``; returns a
@@ -428,14 +436,13 @@ class AssembledCG:
                     break
         else:
             while it < maxiter:
-                nxt = _assembled_step(op, side, st, cur, stream, self.flag)
+                nxt = _assembled_step(op, side, st, cur, stream, self.flag, self.fused)
                 it += 1
                 if it % self.check_every == 0 or it == maxiter:
                     norms.append(float(w.rr[nxt].sqrt().item()))
                     if norms[-1] <= target:
                         converged = True
                         break
-                self._direction(cur, nxt, stream)
                 cur = nxt
         if int(self.flag.item()) & _native.HX_FLAG_NONFINITE:
             raise ValueError("non-finite values during the CG solve")
@@ -443,7 +450,8 @@ class AssembledCG:
 
 
 def cg_solve_assembled(op, side, b, tol=1e-10, maxiter=1000, check_every=10,
-                       mask_boundary=True, work=None, shard=None, graph=False):
+                       mask_boundary=True, work=None, shard=None, graph=False,
+                       fuse_direction=True):
     """Solve the assembled system ``mask Q^T A_L Q x = mask Q^T b`` by CG.
 
     ``op`` is an OperatorInstance on build_cube_mesh(side, extent) (perturbing
@@ -456,25 +464,23 @@ def cg_solve_assembled(op, side, b, tol=1e-10, maxiter=1000, check_every=10,
     global node holds the same value).  Per iteration: the fused matvec +
     <p, A p>, the halo exchange (multi-GPU), the gather-scatter of A p in
     place with three per-axis face passes, the update (plain read of the
-    assembled A p, masked, multiplicity-weighted <r, r>), the direction
-    update.  ``graph=True``: see AssembledCG (capturing costs ~40 ms, so
+    assembled A p, masked, multiplicity-weighted <r, r>); the direction
+    update rides the next matvec (``fuse_direction``, module docstring).
+    ``graph=True``: see AssembledCG (capturing costs ~40 ms, so
     reuse an AssembledCG for repeated solves)."""
-    solver = AssembledCG(op, side, mask_boundary, check_every, shard, graph, work)
+    solver = AssembledCG(op, side, mask_boundary, check_every, shard, graph, work,
+                         fuse_direction)
     return solver.solve(b, tol, maxiter)
 
 
-def cg_iterations_assembled(op, side, b, iterations, work, mask_boundary=True, shard=None):
+def cg_iterations_assembled(op, side, b, iterations, work, mask_boundary=True, shard=None,
+                            fuse_direction=True):
     """``iterations`` assembled-CG steps from x = 0 with no convergence checks
     or host synchronisation (the harness times this)."""
     stream = _stream(op.device)
     st = _AssembledState(op, side, b, mask_boundary, work, shard)
     _assembled_setup(op, side, b, st, stream)
     cur = 0
-    n = b.numel()
-    w = st.w
     for _ in range(iterations):
-        nxt = _assembled_step(op, side, st, cur, stream)
-        _native.lib().hx_cg_direction(_native.ptr(w.p), _native.ptr(w.r), n,
-                                      _native.ptr(w.rr[nxt]), _native.ptr(w.rr[cur]), stream)
-        cur = nxt
+        cur = _assembled_step(op, side, st, cur, stream, None, fuse_direction)
     return st.x

@@ -70,9 +70,10 @@ struct BP1Params {
   int64_t fac_estride;
   int* flag;
   double* energy;  // per-CTA partials of <q, A q> (ENERGY instantiation only)
+  DirArgs dir;     // DIR instantiation: q = r + beta p_old formed in S1 (hx_common.cuh)
 };
 
-template <int N, bool ENERGY>
+template <int N, bool ENERGY, bool DIR = false>
 __global__ void __launch_bounds__(Cfg<kBP1, N>::NT, HX_MINB_BP1_OF(N))
     bp1_kernel(const __grid_constant__ BP1Params<N> p) {
   using C = Cfg<kBP1, N>;
@@ -103,12 +104,14 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT, HX_MINB_BP1_OF(N))
     const int64_t e0 = int64_t(blockIdx.x) * EPB;
     const int64_t ne = min64(EPB, p.n_el - e0);
     prefetch_l2(p.q + HX_QEL(e0) * n3, ne * n3 * sizeof(double));
+    if (DIR) prefetch_l2(p.dir.r + e0 * n3, ne * n3 * sizeof(double));
     prefetch_l2(p.gwj + HX_WEL(e0) * fs, ne * fs * sizeof(double));
     // ... and the second tile's: with back-to-back (PDL) launches this runs
     // under the previous apply's tail (r2_40: +0.4 % at E=32768)
     const int64_t e1 = e0 + int64_t(gridDim.x) * EPB;
     if (e1 < p.n_el) {
       prefetch_l2(p.q + HX_QEL(e1) * n3, min64(EPB, p.n_el - e1) * n3 * sizeof(double));
+      if (DIR) prefetch_l2(p.dir.r + e1 * n3, min64(EPB, p.n_el - e1) * n3 * sizeof(double));
       prefetch_l2(p.gwj + HX_WEL(e1) * fs, min64(EPB, p.n_el - e1) * fs * sizeof(double));
     }
   }
@@ -116,6 +119,8 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT, HX_MINB_BP1_OF(N))
   // PDL (hx_common.cuh): only L2 prefetch hints above this point
   pdl_allow_dependents();
   pdl_wait();
+  double beta = 0.0;
+  if constexpr (DIR) beta = p.dir.rr_new[0] / p.dir.rr_old[0];
 
   double en = 0.0;  // this thread's share of <q, A q> (ENERGY)
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -129,6 +134,7 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT, HX_MINB_BP1_OF(N))
         const int64_t f0 = nt * EPB;
         const int64_t nn = min64(EPB, p.n_el - f0);
         prefetch_l2(p.q + HX_QEL(f0) * n3, nn * n3 * sizeof(double));
+        if (DIR) prefetch_l2(p.dir.r + f0 * n3, nn * n3 * sizeof(double));
         prefetch_l2(p.gwj + HX_WEL(f0) * fs, nn * fs * sizeof(double));
       }
     }
@@ -149,10 +155,8 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT, HX_MINB_BP1_OF(N))
       const int el = g / n2, ln = g % n2;
       if (el >= ne) return;
       const int j = ln / n, i = ln % n;
-      const double* src = p.q + HX_QEL(e0 + el) * n3 + ln;
       double x[n], y[m];
-#pragma unroll
-      for (int t = 0; t < n; ++t) x[t] = src[t * n2];
+      load_line<DIR, n, n2>(p.q, p.dir, beta, HX_QEL(e0 + el) * n3 + ln, x);
       const bool bad = any_nonfinite(x);
       if (bad && p.flag) atomicOr(p.flag, 1);
       fold_apply<m, n, 1>(p.I, x, y);
@@ -251,20 +255,21 @@ __global__ void __launch_bounds__(Cfg<kBP1, N>::NT, HX_MINB_BP1_OF(N))
   }
 }
 
-template <int N, bool E, class Prm>
+template <int N, bool E, bool D = false, class Prm>
 static cudaError_t launch_t(const Prm& prm, int64_t n_el, cudaStream_t s, bool pdl) {
   using C = Cfg<kBP1, N>;
   constexpr int smem = smem_doubles<kBP1, N>() * int(sizeof(double));
   const int64_t ntiles = (n_el + C::EPB - 1) / C::EPB;
   unsigned grid = 0;
-  const cudaError_t err = persistent_grid<bp1_kernel<N, E>>(C::NT, smem, ntiles, &grid);
+  const cudaError_t err = persistent_grid<bp1_kernel<N, E, D>>(C::NT, smem, ntiles, &grid);
   if (err != cudaSuccess) return err;
-  return launch_kernel<bp1_kernel<N, E>>(grid, C::NT, smem, s, pdl, prm);
+  return launch_kernel<bp1_kernel<N, E, D>>(grid, C::NT, smem, s, pdl, prm);
 }
 
 template <int N>
 static cudaError_t launch_n(const hx_plan& P, const double* q, const double* fac, double* out,
-                            int64_t n_el, int* flag, double* energy, cudaStream_t s, bool pdl) {
+                            int64_t n_el, int* flag, double* energy, cudaStream_t s, bool pdl,
+                            const DirArgs* dir) {
   using C = Cfg<kBP1, N>;
   constexpr int n = N + 1, m = N + 2;
   constexpr int smem = smem_doubles<kBP1, N>() * int(sizeof(double));
@@ -280,6 +285,13 @@ static cudaError_t launch_n(const hx_plan& P, const double* q, const double* fac
   prm.fac_estride = P.elem_stride;
   prm.flag = flag;
   prm.energy = energy;
+  if (dir) {  // the CG direction form exists only with the energy epilogue (hx_apply_energy_dir)
+    if (!energy) return cudaErrorInvalidValue;
+    prm.q = dir->p;
+    prm.dir = *dir;
+    return launch_t<N, true, true>(prm, n_el, s, pdl);
+  }
+  prm.dir = DirArgs{};
   return energy ? launch_t<N, true>(prm, n_el, s, pdl) : launch_t<N, false>(prm, n_el, s, pdl);
 }
 
@@ -297,11 +309,12 @@ bool bp1_gwj_cfast(int degree) {
 }
 
 cudaError_t launch_bp1(const hx_plan& P, const double* q, const double* fac, double* out,
-                       int64_t n_el, int* flag, double* energy, cudaStream_t s, bool pdl) {
+                       int64_t n_el, int* flag, double* energy, cudaStream_t s, bool pdl,
+                       const DirArgs* dir) {
   switch (P.degree) {
 #define HX_CASE(N) \
   case N:          \
-    return launch_n<N>(P, q, fac, out, n_el, flag, energy, s, pdl);
+    return launch_n<N>(P, q, fac, out, n_el, flag, energy, s, pdl, dir);
     HX_CASE(1) HX_CASE(2) HX_CASE(3) HX_CASE(4) HX_CASE(5) HX_CASE(6) HX_CASE(7) HX_CASE(8)
     HX_CASE(9) HX_CASE(10) HX_CASE(11) HX_CASE(12) HX_CASE(13) HX_CASE(14) HX_CASE(15)
 #undef HX_CASE

@@ -47,9 +47,10 @@ struct BP35Params {
   double lam;
   int* flag;
   double* energy;  // per-CTA partials of <q, A q> (ENERGY instantiation only)
+  DirArgs dir;     // DIR instantiation: q = r + beta p_old formed in S1 (hx_common.cuh)
 };
 
-template <int N, bool ENERGY>
+template <int N, bool ENERGY, bool DIR = false>
 __global__ void __launch_bounds__(Cfg<kBP35, N>::NT, HX_MINB_BP35_OF(N))
     bp35_kernel(const __grid_constant__ BP35Params<N> p) {
   using C = Cfg<kBP35, N>;
@@ -77,11 +78,14 @@ __global__ void __launch_bounds__(Cfg<kBP35, N>::NT, HX_MINB_BP35_OF(N))
     const int64_t e0 = int64_t(blockIdx.x) * EPB;
     const int64_t ne = min64(EPB, p.n_el - e0);
     prefetch_l2(p.q + e0 * n3, ne * n3 * sizeof(double));
+    if (DIR) prefetch_l2(p.dir.r + e0 * n3, ne * n3 * sizeof(double));
   }
 
   // PDL (hx_common.cuh): only L2 prefetch hints above this point
   pdl_allow_dependents();
   pdl_wait();
+  double beta = 0.0;
+  if constexpr (DIR) beta = p.dir.rr_new[0] / p.dir.rr_old[0];
 
   double en = 0.0;  // this thread's share of <q, A q> (ENERGY)
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -105,10 +109,8 @@ __global__ void __launch_bounds__(Cfg<kBP35, N>::NT, HX_MINB_BP35_OF(N))
     // ---- S1: k-lines over (j, i)
     if (act) {
       const int j = ln / n, i = ln % n;
-      const double* src = p.q + e * n3 + j * n + i;
       double qk[n];
-#pragma unroll
-      for (int k = 0; k < n; ++k) qk[k] = src[k * n2];
+      load_line<DIR, n, n2>(p.q, p.dir, beta, e * n3 + j * n + i, qk);
       const bool bad = any_nonfinite(qk);
       if (bad && p.flag) atomicOr(p.flag, 1);
       if constexpr (!kLean) {
@@ -149,6 +151,7 @@ __global__ void __launch_bounds__(Cfg<kBP35, N>::NT, HX_MINB_BP35_OF(N))
       if (nt < ntiles) {
         const int64_t f0 = nt * EPB;
         prefetch_l2(p.q + f0 * n3, min64(EPB, p.n_el - f0) * n3 * sizeof(double));
+        if (DIR) prefetch_l2(p.dir.r + f0 * n3, min64(EPB, p.n_el - f0) * n3 * sizeof(double));
       }
     }
     if (act) {
@@ -237,20 +240,21 @@ __global__ void __launch_bounds__(Cfg<kBP35, N>::NT, HX_MINB_BP35_OF(N))
   }
 }
 
-template <int N, bool E, class Prm>
+template <int N, bool E, bool D = false, class Prm>
 static cudaError_t launch_t(const Prm& prm, int64_t n_el, cudaStream_t s, bool pdl) {
   using C = Cfg<kBP35, N>;
   constexpr int smem = smem_doubles<kBP35, N>() * int(sizeof(double));
   const int64_t ntiles = (n_el + C::EPB - 1) / C::EPB;
   unsigned grid = 0;
-  const cudaError_t err = persistent_grid<bp35_kernel<N, E>>(C::NT, smem, ntiles, &grid);
+  const cudaError_t err = persistent_grid<bp35_kernel<N, E, D>>(C::NT, smem, ntiles, &grid);
   if (err != cudaSuccess) return err;
-  return launch_kernel<bp35_kernel<N, E>>(grid, C::NT, smem, s, pdl, prm);
+  return launch_kernel<bp35_kernel<N, E, D>>(grid, C::NT, smem, s, pdl, prm);
 }
 
 template <int N>
 static cudaError_t launch_n(const hx_plan& P, const double* q, const double* fac, double* out,
-                            int64_t n_el, int* flag, double* energy, cudaStream_t s, bool pdl) {
+                            int64_t n_el, int* flag, double* energy, cudaStream_t s, bool pdl,
+                            const DirArgs* dir) {
   BP35Params<N> prm;
   constexpr int n = N + 1;
   double dt[n * n];
@@ -266,15 +270,23 @@ static cudaError_t launch_n(const hx_plan& P, const double* q, const double* fac
   prm.lam = P.lam;
   prm.flag = flag;
   prm.energy = energy;
+  if (dir) {  // the CG direction form exists only with the energy epilogue (hx_apply_energy_dir)
+    if (!energy) return cudaErrorInvalidValue;
+    prm.q = dir->p;
+    prm.dir = *dir;
+    return launch_t<N, true, true>(prm, n_el, s, pdl);
+  }
+  prm.dir = DirArgs{};
   return energy ? launch_t<N, true>(prm, n_el, s, pdl) : launch_t<N, false>(prm, n_el, s, pdl);
 }
 
 cudaError_t launch_bp35(const hx_plan& P, const double* q, const double* fac, double* out,
-                        int64_t n_el, int* flag, double* energy, cudaStream_t s, bool pdl) {
+                        int64_t n_el, int* flag, double* energy, cudaStream_t s, bool pdl,
+                        const DirArgs* dir) {
   switch (P.degree) {
 #define HX_CASE(N) \
   case N:          \
-    return launch_n<N>(P, q, fac, out, n_el, flag, energy, s, pdl);
+    return launch_n<N>(P, q, fac, out, n_el, flag, energy, s, pdl, dir);
     HX_CASE(1) HX_CASE(2) HX_CASE(3) HX_CASE(4) HX_CASE(5) HX_CASE(6) HX_CASE(7) HX_CASE(8)
     HX_CASE(9) HX_CASE(10) HX_CASE(11) HX_CASE(12) HX_CASE(13) HX_CASE(14) HX_CASE(15)
 #undef HX_CASE

@@ -49,15 +49,16 @@ static int kernel_shape(int bp, int degree, int* epb, int* nt, int* smem) {
 }
 
 cudaError_t launch_apply(const hx_plan& P, const double* q, const double* fac, double* out,
-                         int64_t n_el, int* flag, cudaStream_t s, double* energy, bool pdl) {
+                         int64_t n_el, int* flag, cudaStream_t s, double* energy, bool pdl,
+                         const DirArgs* dir) {
   if (n_el == 0) return cudaSuccess;
   switch (P.bp) {
     case HX_BP1:
-      return launch_bp1(P, q, fac, out, n_el, flag, energy, s, pdl);
+      return launch_bp1(P, q, fac, out, n_el, flag, energy, s, pdl, dir);
     case HX_BP35:
-      return launch_bp35(P, q, fac, out, n_el, flag, energy, s, pdl);
+      return launch_bp35(P, q, fac, out, n_el, flag, energy, s, pdl, dir);
     default:
-      return launch_bp3(P, q, fac, out, n_el, flag, energy, s, pdl);
+      return launch_bp3(P, q, fac, out, n_el, flag, energy, s, pdl, dir);
   }
 }
 
@@ -446,6 +447,24 @@ int hx_apply_energy(const hx_plan* P, const double* q, const double* factors, do
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   cudaError_t err = cudaMemsetAsync(partials, 0, sizeof(double) * n_partials, s);
   if (err == cudaSuccess) err = launch_apply(*P, q, factors, out, n_el, flag, s, partials, kApplyPdl);
+  if (err == cudaSuccess) err = launch_sum(partials, int(n_partials), energy, s);
+  return cuda_status(err);
+}
+
+int hx_apply_energy_dir(const hx_plan* P, double* p, const double* r, const double* rr_new,
+                        const double* rr_old, const double* factors, double* out, int64_t n_el,
+                        double* partials, int64_t n_partials, double* energy, int* flag,
+                        void* stream) {
+  if (!P || n_el < 0 || !partials || !energy || !rr_new || !rr_old) return HX_EINVAL;
+  if (n_el > 0 && (!p || !r || !factors || !out || p == r || out == p || out == r))
+    return HX_EINVAL;
+  if (n_partials < hx_energy_partials()) return HX_EINVAL;
+  hx::NvtxRange range(hx::range_name(*P, "energy"));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const DirArgs dir{p, r, rr_new, rr_old};
+  cudaError_t err = cudaMemsetAsync(partials, 0, sizeof(double) * n_partials, s);
+  if (err == cudaSuccess)
+    err = launch_apply(*P, p, factors, out, n_el, flag, s, partials, kApplyPdl, &dir);
   if (err == cudaSuccess) err = launch_sum(partials, int(n_partials), energy, s);
   return cuda_status(err);
 }

@@ -215,6 +215,37 @@ inline cudaError_t resident_blocks(int threads, int smem, int* blocks) {
   return cudaSuccess;
 }
 
+// CG search-direction update fused into a matvec's first load
+// (hx_apply_energy_dir): the kernel reads p_old and r where it would read q,
+// forms p = r + beta p_old with beta = rr_new / rr_old -- hx_cg_direction's
+// formula, bit for bit -- stores p back and applies the operator to it, so
+// the direction update costs no pass of its own (DirArgs: hx_plan.h).
+// Load one line of q, or (DIR) form and store the line of p = r + beta p_old.
+template <bool DIR, int L, int STRIDE, class Dir>
+__device__ __forceinline__ void load_line(const double* q, const Dir& d, double beta,
+                                          int64_t off, double (&x)[L]) {
+  if constexpr (DIR) {
+    // all loads before any store: the stores may alias the loads as far as
+    // the compiler knows, and interleaving them would serialise the line's
+    // 2L loads into L dependent round trips
+    const double* __restrict__ pp = d.p + off;
+    const double* __restrict__ rp = d.r + off;
+    double pv[L];
+#pragma unroll
+    for (int t = 0; t < L; ++t) {
+      pv[t] = pp[t * STRIDE];
+      x[t] = rp[t * STRIDE];
+    }
+#pragma unroll
+    for (int t = 0; t < L; ++t) x[t] = fma(beta, pv[t], x[t]);
+#pragma unroll
+    for (int t = 0; t < L; ++t) d.p[off + int64_t(t) * STRIDE] = x[t];
+  } else {
+#pragma unroll
+    for (int t = 0; t < L; ++t) x[t] = q[off + int64_t(t) * STRIDE];
+  }
+}
+
 // Programmatic dependent launch (PDL).  A persistent element kernel launched
 // with cudaLaunchAttributeProgrammaticStreamSerialization may start while
 // the previous kernel of the stream is still retiring its last CTAs: it only

@@ -51,11 +51,21 @@ struct hx_plan {
 
 namespace hx {
 
+// CG direction fused into the matvec's first load (hx_common.cuh load_line):
+// the kernel forms p = r + (rr_new / rr_old) p, stores it and applies A to it
+struct DirArgs {
+  double* p;
+  const double* r;
+  const double* rr_new;
+  const double* rr_old;
+};
+
 // the fused kernel of the plan's operator (energy: per-CTA <q, A q> partials)
 // (pdl: as a programmatic dependent launch, hx_common.cuh launch_kernel)
+// (dir: q is ignored and the operator applies to the updated direction)
 cudaError_t launch_apply(const hx_plan& P, const double* q, const double* fac, double* out,
                          int64_t n_el, int* flag, cudaStream_t s, double* energy = nullptr,
-                         bool pdl = false);
+                         bool pdl = false, const DirArgs* dir = nullptr);
 // host pipeline helpers (hx_capi.cu): chunk sizes, lazily built streams
 std::vector<int64_t> chunk_schedule(int64_t n_el, int64_t chunk_el);
 cudaError_t pipe_setup(hx_plan* P);
@@ -71,11 +81,14 @@ __host__ __device__ inline int bp1_gwj_index(int k, int j, int i, int m, bool cf
 
 // launch the fused element kernel for elements [0, n_el) of device arrays
 cudaError_t launch_bp1(const hx_plan& P, const double* q, const double* fac, double* out,
-                       int64_t n_el, int* flag, double* energy, cudaStream_t s, bool pdl);
+                       int64_t n_el, int* flag, double* energy, cudaStream_t s, bool pdl,
+                       const DirArgs* dir);
 cudaError_t launch_bp35(const hx_plan& P, const double* q, const double* fac, double* out,
-                        int64_t n_el, int* flag, double* energy, cudaStream_t s, bool pdl);
+                        int64_t n_el, int* flag, double* energy, cudaStream_t s, bool pdl,
+                        const DirArgs* dir);
 cudaError_t launch_bp3(const hx_plan& P, const double* q, const double* fac, double* out,
-                       int64_t n_el, int* flag, double* energy, cudaStream_t s, bool pdl);
+                       int64_t n_el, int* flag, double* energy, cudaStream_t s, bool pdl,
+                       const DirArgs* dir);
 cudaError_t launch_baseline(const hx_plan& P, const double* q, const double* fac, double* out,
                             int64_t n_el, double* work, int* flag, cudaStream_t s);
 int64_t baseline_workspace_doubles(const hx_plan& P, int64_t n_el);

@@ -280,3 +280,19 @@ def test_graphed_assembled_cg_is_bitwise_the_eager_one():
     assert graphed.iterations == -(-eager.iterations // 10) * 10
     # the eager solve stopped at its check; the graphed one at the same check
     np.testing.assert_array_equal(graphed.x.cpu().numpy(), eager.x.cpu().numpy())
+
+
+@pytest.mark.parametrize("bp", [hx.BP1, hx.BP35, hx.BP3])
+def test_assembled_cg_fused_direction_bitwise(bp):
+    """The direction update fused into the matvec (hx_apply_energy_dir) gives
+    the unfused assembled iterates bit for bit, eager and graphed."""
+    side, deg = 3, 5
+    mesh = hx.build_cube_mesh(side, 2.0)
+    op = hx.make_operator(bp, deg, mesh, lam=0.0 if bp != hx.BP1 else 1.0)
+    b = torch.from_numpy(np.random.default_rng(5).standard_normal((mesh.n_el, op.n_p))).cuda()
+    fused = cg_solve_assembled(op, side, b, tol=1e-11, check_every=10)
+    plain = cg_solve_assembled(op, side, b, tol=1e-11, check_every=10, fuse_direction=False)
+    assert fused.converged and fused.iterations == plain.iterations
+    np.testing.assert_array_equal(fused.x.cpu().numpy(), plain.x.cpu().numpy())
+    graphed = cg_solve_assembled(op, side, b, tol=1e-11, check_every=10, graph=True)
+    np.testing.assert_array_equal(graphed.x.cpu().numpy(), fused.x.cpu().numpy())

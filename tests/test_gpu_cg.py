@@ -149,3 +149,83 @@ def test_graphed_element_local_cg_bitwise(mesh3):
     graphed = cg_solve(op, b, tol=1e-11, check_every=10, graph=True)
     assert eager.converged and graphed.converged and graphed.iterations == eager.iterations
     np.testing.assert_array_equal(graphed.x.cpu().numpy(), eager.x.cpu().numpy())
+
+
+@pytest.mark.parametrize("bp", BPS)
+@pytest.mark.parametrize("deg", [1, 2, 7, 10, 13])
+def test_apply_energy_dir_matches_unfused(bp, deg, mesh3):
+    """hx_apply_energy_dir == hx_cg_direction then hx_apply_energy, bit for bit
+    (p, A p and <p, A p>), on a mesh of more tiles than one CTA covers."""
+    mesh = hx.perturb_mesh(hx.build_cube_mesh(5 if deg < 10 else 3, 2.0), 0.1, seed=deg)
+    op = hx.make_operator(bp, deg, mesh, lam=0.7)
+    g = torch.Generator("cuda").manual_seed(deg)
+    shape = (op.n_el, op.n_p)
+    p0 = torch.randn(shape, dtype=torch.float64, device="cuda", generator=g)
+    r = torch.randn(shape, dtype=torch.float64, device="cuda", generator=g)
+    rr = torch.tensor([1.7, 0.3], dtype=torch.float64, device="cuda")
+    L = _native.lib()
+    npart = L.hx_energy_partials()
+    part = torch.empty(npart, dtype=torch.float64, device="cuda")
+    outs = []
+    for fused in (False, True):
+        p = p0.clone()
+        ap = torch.full_like(p, float("nan"))
+        en = torch.zeros(1, dtype=torch.float64, device="cuda")
+        flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+        if fused:
+            _native.check(L.hx_apply_energy_dir(
+                op.plan.handle, p.data_ptr(), r.data_ptr(), rr[0:1].data_ptr(),
+                rr[1:2].data_ptr(), op.device_factors.data_ptr(), ap.data_ptr(), op.n_el,
+                part.data_ptr(), npart, en.data_ptr(), flag.data_ptr(), None))
+        else:
+            _native.check(L.hx_cg_direction(p.data_ptr(), r.data_ptr(), p.numel(),
+                                            rr[0:1].data_ptr(), rr[1:2].data_ptr(), None))
+            _native.check(L.hx_apply_energy(op.plan.handle, p.data_ptr(),
+                                            op.device_factors.data_ptr(), ap.data_ptr(),
+                                            op.n_el, part.data_ptr(), npart, en.data_ptr(),
+                                            flag.data_ptr(), None))
+        torch.cuda.synchronize()
+        assert int(flag.item()) == 0
+        outs.append((p, ap, en))
+    (pu, apu, enu), (pf, apf, enf) = outs
+    assert torch.equal(pf, pu) and torch.equal(apf, apu) and torch.equal(enf, enu)
+    beta = 1.7 / 0.3
+    torch.testing.assert_close(pf, r + beta * p0, rtol=1e-15, atol=1e-15)
+
+
+def test_apply_energy_dir_rejects_aliasing(mesh3):
+    op = hx.make_operator(hx.BP35, 3, mesh3)
+    L = _native.lib()
+    npart = L.hx_energy_partials()
+    part = torch.empty(npart, dtype=torch.float64, device="cuda")
+    v = torch.zeros(op.n_el, op.n_p, dtype=torch.float64, device="cuda")
+    u = torch.zeros_like(v)
+    s = torch.ones(2, dtype=torch.float64, device="cuda")
+    f = op.device_factors.data_ptr()
+
+    def call(p, r, out, n=op.n_el, rr=s.data_ptr()):
+        return L.hx_apply_energy_dir(op.plan.handle, p, r, rr, rr, f, out, n, part.data_ptr(),
+                                     npart, s.data_ptr(), None, None)
+
+    e = _native.HX_EINVAL
+    assert call(v.data_ptr(), v.data_ptr(), u.data_ptr()) == e  # p == r
+    assert call(v.data_ptr(), u.data_ptr(), v.data_ptr()) == e  # out == p
+    assert call(v.data_ptr(), u.data_ptr(), u.data_ptr()) == e  # out == r
+    assert call(v.data_ptr(), u.data_ptr(), part.data_ptr(), rr=None) == e
+    assert call(None, None, None, n=0) == _native.HX_OK
+
+
+@pytest.mark.parametrize("bp", BPS)
+def test_cg_fused_direction_bitwise(bp, mesh3):
+    """The fused iteration produces the unfused iterates bit for bit."""
+    op = hx.make_operator(bp, 4, mesh3, lam=0.9)
+    b = torch.from_numpy(np.random.default_rng(11).standard_normal((27, op.n_p))).cuda()
+    w = CGWorkspace(b)
+    xf = cg_iterations(op, b, 17, w).clone()
+    xu = cg_iterations(op, b, 17, w, fuse_direction=False)
+    torch.cuda.synchronize()
+    assert torch.equal(xf, xu)
+    a = cg_solve(op, b, tol=1e-11, check_every=5)
+    u = cg_solve(op, b, tol=1e-11, check_every=5, fuse_direction=False)
+    assert a.converged and a.iterations == u.iterations
+    np.testing.assert_array_equal(a.x.cpu().numpy(), u.x.cpu().numpy())
