@@ -35,6 +35,20 @@
 #ifndef HX_BP3_REREAD_MIN_N
 #define HX_BP3_REREAD_MIN_N 7
 #endif
+// S5: points of factors loaded ahead into a register ring (0: at use);
+// HX_BP3_FPF overrides the per-degree choice for degrees >= HX_BP3_FPF_MIN_N
+// (experiments).  Measured (r2_53, config 4): +0.02 at N=11 (2 points) and
+// N=14 (1 point), no change elsewhere.
+#ifndef HX_BP3_FPF_MIN_N
+#define HX_BP3_FPF_MIN_N 16
+#endif
+template <int N>
+constexpr int bp3_fpf() {
+#ifdef HX_BP3_FPF
+  if (N >= HX_BP3_FPF_MIN_N) return HX_BP3_FPF;
+#endif
+  return N == 11 ? 2 : N == 14 ? 1 : 0;
+}
 #ifndef HX_PF_BP3
 #define HX_PF_BP3 2  // stage at which a tile's factors are prefetched into L2
 #endif
@@ -178,6 +192,31 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT, HX_MINB_BP3_OF(N))
     const int ca = ln_c / m, cc = ln_c % m;
     const double* const gfac = p.fac + HX_WEL(e0 + el_c) * fs + ln_c;
     auto fac_at = [&](int t, int sl) -> double { return gfac[t * m2 + sl * ss]; };
+    // S5's seven factors of point t, optionally from a register ring filled
+    // kFpf points ahead (latency of the L2-resident factor loads)
+    constexpr int kFpf = bp3_fpf<N>();
+    double fring[kFpf > 0 ? kFpf : 1][7];
+    auto fac7 = [&](int t, double (&g)[7]) {
+      if constexpr (kFpf > 0) {
+#pragma unroll
+        for (int sl = 0; sl < 7; ++sl) g[sl] = fring[t % kFpf][sl];
+        if (t + kFpf < m) {
+#pragma unroll
+          for (int sl = 0; sl < 7; ++sl) fring[t % kFpf][sl] = fac_at(t + kFpf, sl);
+        }
+      } else {
+#pragma unroll
+        for (int sl = 0; sl < 7; ++sl) g[sl] = fac_at(t, sl);
+      }
+    };
+    auto fac_ring_start = [&]() {
+      if constexpr (kFpf > 0) {
+#pragma unroll
+        for (int u = 0; u < kFpf; ++u)
+#pragma unroll
+          for (int sl = 0; sl < 7; ++sl) fring[u][sl] = u < m ? fac_at(u, sl) : 0.0;
+      }
+    };
     if (act_c) {
       const double* src = Bc + ca * LY.s1 + cc;
       double x[n], tv[m];
@@ -229,6 +268,7 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT, HX_MINB_BP3_OF(N))
         double* qsl = Bc + ca * LQS.s1 + cc;
         double* tl = Cc + ca * LT.s1 + cc;
         double tt[m], rqt[m];
+        fac_ring_start();
         {
           double tv[m];
 #pragma unroll
@@ -237,9 +277,11 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT, HX_MINB_BP3_OF(N))
         }
 #pragma unroll
         for (int t = 0; t < m; ++t) {
-          const double grr = fac_at(t, 0), grs = fac_at(t, 1), grt = fac_at(t, 2);
-          const double gss = fac_at(t, 3), gst = fac_at(t, 4), gtt = fac_at(t, 5);
-          const double gwj = fac_at(t, 6);
+          double g[7];
+          fac7(t, g);
+          const double grr = g[0], grs = g[1], grt = g[2];
+          const double gss = g[3], gst = g[4], gtt = g[5];
+          const double gwj = g[6];
           const double qr = qrl[LQR.kofs(t)], qs = qsl[LQS.kofs(t)], qt = tt[t];
           const double tvt = tl[LT.kofs(t)];
           const double rqr = grr * qr + grs * qs + grt * qt;
@@ -260,6 +302,7 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT, HX_MINB_BP3_OF(N))
       double* qrl = Ac + ca * LQR.s1 + cc;
       double* qsl = Bc + ca * LQS.s1 + cc;
       double rqt[m], tv[m], tt[m];
+      fac_ring_start();
       if constexpr (kReread) {
         // re-read this thread's own T k-line (still intact in C)
         const double* tl = Cc + ca * LT.s1 + cc;
@@ -275,9 +318,11 @@ __global__ void __launch_bounds__(Cfg<kBP3, N>::NT, HX_MINB_BP3_OF(N))
       }
 #pragma unroll
       for (int t = 0; t < m; ++t) {
-        const double grr = fac_at(t, 0), grs = fac_at(t, 1), grt = fac_at(t, 2);
-        const double gss = fac_at(t, 3), gst = fac_at(t, 4), gtt = fac_at(t, 5);
-        const double gwj = fac_at(t, 6);
+        double g[7];
+        fac7(t, g);
+        const double grr = g[0], grs = g[1], grt = g[2];
+        const double gss = g[3], gst = g[4], gtt = g[5];
+        const double gwj = g[6];
         const double qr = qrl[LQR.kofs(t)], qs = qsl[LQS.kofs(t)], qt = tt[t];
         const double rqr = grr * qr + grs * qs + grt * qt;
         const double rqs = grs * qr + gss * qs + gst * qt;
