@@ -56,6 +56,11 @@ BP1_CFAST = _degrees("HX_GEN_BP1_CFAST", {2, 4, 6, 8, 10, 12, 14})
 # (ORD bit 8), chosen by the model against the default (r2_26: N=4 0.84 ->
 # 0.87, N=6 0.90 -> 0.92, N=8 0.78 -> 0.79, N=10 0.70 -> 0.72)
 BP3_KI = _degrees("HX_GEN_BP3_KI", {2, 4, 6, 8, 10, 12, 14})
+# BP3.0 degrees whose S2 / S8 i-lines may take the k-paired lane order (ORD
+# 4, conflict-free X / Y / Z at N=7 in the model).  Round 1 measured it 1-2 %
+# slower at N=7 (r11/r12); on the round-2 kernel it is +0.2 % at E=32768 and
+# E=97,336 (r2_59: shared wavefronts 40.5 M -> 38.9 M, conflicts 4.6 M -> 2.8 M)
+BP3_ORD4 = _degrees("HX_GEN_BP3_ORD4", {7})
 # BP3.0 degrees whose layouts weight each access pattern by the number of
 # passes that use it (phases()) instead of counting every pattern once
 # (r2_16: N=10 0.687 -> 0.706, N=12 0.598 -> 0.613, equal elsewhere; at
@@ -273,6 +278,8 @@ def plan(bp, deg, target=TARGET_THREADS, qstage=False):
     ords = {BP1: (0, 2, 4), INTERP: (0, 2, 4)}.get(bp, (0,))
     if bp == BP3 and m % 2 == 0 and deg in BP3_KI:
         ords = (0, 8)
+    if bp == BP3 and deg in BP3_ORD4:
+        ords = ords + (4,)
     if bp == BP1 and deg in BP1_CFAST:
         ords = ords + tuple(o | 8 for o in ords)
     best = None
