@@ -272,9 +272,8 @@ def plan(bp, deg, target=TARGET_THREADS, qstage=False):
         # BP1.0 only: a CTA smaller than one element's line count walks over
         # the lines (for_lines); one element per tile
         nt = max(32, -(-target // 32) * 32)
-    # BP3.0 supports ORD 4 too, but it measured 1-2 % slower at N=7 despite
-    # fewer conflicts (r11/r12: latency-bound, not shared-memory-bound), so
-    # the search stays on the default order there
+    # BP3.0: ORD 4 only for the BP3_ORD4 degrees (N=7: +0.2 %, r2_59; round
+    # 1 measured it 1-2 % slower, r11/r12), ORD 8 for BP3_KI
     ords = {BP1: (0, 2, 4), INTERP: (0, 2, 4)}.get(bp, (0,))
     if bp == BP3 and m % 2 == 0 and deg in BP3_KI:
         ords = (0, 8)
