@@ -15,6 +15,10 @@
 //   S4 i-lines: B <- D_r^T B                 j-lines: C <- D_s^T C
 //   S5 k-lines (j,i): out = acc + B + C (HBM, coalesced)
 //
+// Cfg::ORD (tools/gen_layouts.py BP35_ORD degrees): S2 / S4 enumerate their
+// (k, r) lines k-fastest (2) or k-paired (4, with k-paired layouts) instead
+// of r-fastest; the k-line stages touch HBM and keep (j, i) i-fastest lanes.
+//
 // The only HBM traffic is q, the 7 factor slots and out (Table 1: 9 n^3
 // doubles per element).  Inputs are pulled into L2 ahead of use with bulk
 // prefetches (schedule below), so the loads in S1/S3 hit L2.
@@ -120,27 +124,28 @@ __global__ void __launch_bounds__(Cfg<kBP35, N>::NT, HX_MINB_BP35_OF(N))
       }
       double* a = Ae + j * LA.s1 + i;
 #pragma unroll
-      for (int k = 0; k < n; ++k) a[k * LA.s0] = qk[k];
+      for (int k = 0; k < n; ++k) a[LA.kofs(k)] = qk[k];
     }
     __syncthreads();
     // ---- S2: r- and s-derivatives
     if (HX_PF_BP35 == 2 && tid == 0)
       prefetch_l2(p.fac + e0 * p.fac_estride, ne * p.fac_estride * sizeof(double));
     if (act) {
-      const int k = ln / n, r = ln % n;
+      int k, r;  // Cfg::ORD: lane order over (k, r) (hx_common.cuh iline_coords)
+      iline_coords<n, n, (C::ORD & 6)>(ln, k, r);
       double x[n], y[n];
-      const double* a = Ae + k * LA.s0 + r * LA.s1;  // i-line (k, j=r)
+      const double* a = Ae + LA.kofs(k) + r * LA.s1;  // i-line (k, j=r)
 #pragma unroll
       for (int t = 0; t < n; ++t) x[t] = a[t];
       fold_apply<n, n, -1>(p.D, x, y);
-      double* b = Be + k * LB.s0 + r * LB.s1;
+      double* b = Be + LB.kofs(k) + r * LB.s1;
 #pragma unroll
       for (int t = 0; t < n; ++t) b[t] = y[t];
-      a = Ae + k * LA.s0 + r;  // j-line (k, i=r)
+      a = Ae + LA.kofs(k) + r;  // j-line (k, i=r)
 #pragma unroll
       for (int t = 0; t < n; ++t) x[t] = a[t * LA.s1];
       fold_apply<n, n, -1>(p.D, x, y);
-      double* c = Ce + k * LC.s0 + r;
+      double* c = Ce + LC.kofs(k) + r;
 #pragma unroll
       for (int t = 0; t < n; ++t) c[t * LC.s1] = y[t];
     }
@@ -164,7 +169,7 @@ __global__ void __launch_bounds__(Cfg<kBP35, N>::NT, HX_MINB_BP35_OF(N))
       if constexpr (kLean) {
         double x[n];
 #pragma unroll
-        for (int k = 0; k < n; ++k) x[k] = a[k * LA.s0];
+        for (int k = 0; k < n; ++k) x[k] = a[LA.kofs(k)];
         fold_apply<n, n, -1>(p.D, x, qtl);
       }
 #pragma unroll
@@ -173,18 +178,18 @@ __global__ void __launch_bounds__(Cfg<kBP35, N>::NT, HX_MINB_BP35_OF(N))
         const double grr = gk[0], grs = gk[ss], grt = gk[2 * ss];
         const double gss = gk[3 * ss], gst = gk[4 * ss], gtt = gk[5 * ss];
         const double gwj = gk[6 * ss];
-        const double qk = kLean ? a[k * LA.s0] : qv[k];
-        const double qr = b[k * LB.s0], qs = c[k * LC.s0], qtk = kLean ? qtl[k] : qt[k];
+        const double qk = kLean ? a[LA.kofs(k)] : qv[k];
+        const double qr = b[LB.kofs(k)], qs = c[LC.kofs(k)], qtk = kLean ? qtl[k] : qt[k];
         const double rqr = grr * qr + grs * qs + grt * qtk;
         const double rqs = grs * qr + gss * qs + gst * qtk;
-        b[k * LB.s0] = rqr;
-        c[k * LC.s0] = rqs;
+        b[LB.kofs(k)] = rqr;
+        c[LC.kofs(k)] = rqs;
         rqt[k] = grt * qr + gst * qs + gtt * qtk;
         const double lq = p.lam * gwj * qk;
         // <q, A q> = sum over points of grad q . G grad q + lam GwJ q^2
         if constexpr (ENERGY) en += qr * rqr + qs * rqs + qtk * rqt[k] + qk * lq;
         if constexpr (kLean)
-          a[k * LA.s0] = lq;
+          a[LA.kofs(k)] = lq;
         else
           qv[k] = lq;
       }
@@ -192,7 +197,7 @@ __global__ void __launch_bounds__(Cfg<kBP35, N>::NT, HX_MINB_BP35_OF(N))
         double ac[n];
         fold_apply<n, n, -1>(p.Dt, rqt, ac);
 #pragma unroll
-        for (int k = 0; k < n; ++k) a[k * LA.s0] += ac[k];
+        for (int k = 0; k < n; ++k) a[LA.kofs(k)] += ac[k];
       } else {
         fold_apply<n, n, -1>(p.Dt, rqt, acc);
 #pragma unroll
@@ -202,15 +207,16 @@ __global__ void __launch_bounds__(Cfg<kBP35, N>::NT, HX_MINB_BP35_OF(N))
     __syncthreads();
     // ---- S4: transposed r- and s-derivatives, in place
     if (act) {
-      const int k = ln / n, r = ln % n;
+      int k, r;
+      iline_coords<n, n, (C::ORD & 6)>(ln, k, r);
       double x[n], y[n];
-      double* b = Be + k * LB.s0 + r * LB.s1;
+      double* b = Be + LB.kofs(k) + r * LB.s1;
 #pragma unroll
       for (int t = 0; t < n; ++t) x[t] = b[t];
       fold_apply<n, n, -1>(p.Dt, x, y);
 #pragma unroll
       for (int t = 0; t < n; ++t) b[t] = y[t];
-      double* c = Ce + k * LC.s0 + r;
+      double* c = Ce + LC.kofs(k) + r;
 #pragma unroll
       for (int t = 0; t < n; ++t) x[t] = c[t * LC.s1];
       fold_apply<n, n, -1>(p.Dt, x, y);
@@ -227,7 +233,7 @@ __global__ void __launch_bounds__(Cfg<kBP35, N>::NT, HX_MINB_BP35_OF(N))
       const double* a = Ae + j * LA.s1 + i;
 #pragma unroll
       for (int k = 0; k < n; ++k)
-        st_stream(dst + k * n2, (kLean ? a[k * LA.s0] : acc[k]) + b[k * LB.s0] + c[k * LC.s0]);
+        st_stream(dst + k * n2, (kLean ? a[LA.kofs(k)] : acc[k]) + b[LB.kofs(k)] + c[LC.kofs(k)]);
     }
     // A is rewritten by the next tile's S1 only after it has passed this
     // tile's S3/S4 barriers (with kLean, S5 reads only the thread's own

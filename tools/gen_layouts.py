@@ -61,6 +61,11 @@ BP3_KI = _degrees("HX_GEN_BP3_KI", {2, 4, 6, 8, 10, 12, 14})
 # slower at N=7 (r11/r12); on the round-2 kernel it is +0.2 % at E=32768 and
 # E=97,336 (r2_59: shared wavefronts 40.5 M -> 38.9 M, conflicts 4.6 M -> 2.8 M)
 BP3_ORD4 = _degrees("HX_GEN_BP3_ORD4", {7})
+# BP3.5 degrees whose S2 / S4 lines may take the k-fastest (ORD 2) or
+# k-paired (ORD 4, k-paired layouts) lane order; the k-line stages touch HBM
+# and keep i-fastest lanes.  Measured (r2_60, config 4): N=9 0.975 -> 0.985,
+# N=11 0.875 -> 0.925, N=13 0.795 -> 0.868; flat at every other degree
+BP35_ORD = _degrees("HX_GEN_BP35_ORD", {9, 11, 13})
 # BP3.0 degrees whose layouts weight each access pattern by the number of
 # passes that use it (phases()) instead of counting every pattern once
 # (r2_16: N=10 0.687 -> 0.706, N=12 0.598 -> 0.613, equal elsewhere; at
@@ -194,8 +199,13 @@ def _best_layout(d, pats, paired=False, wide=False):
 def phases(bp, n, m, ord_=0):
     """(buffer id, dims, patterns) for every tensor phase of a kernel."""
     if bp == BP35:
-        return [(0, (n, n, n), (0, 1, 2)), (1, (n, n, n), (0, 2)),
-                (2, (n, n, n), (0, 1))]
+        # A: S1 / S3 / S5 k-lines (0), S2 j-lines and i-lines; B: S2 / S4
+        # i-lines; C: S2 / S4 j-lines.  ORD: lane order over (k, r) in S2 / S4
+        # -- 0 r fastest (j-lines 1, i-lines 2), 2 k fastest (4, 5), 4
+        # k-paired (7, 6)
+        pj, pi = {0: (1, 2), 2: (4, 5), 4: (7, 6)}[ord_ & 6]
+        return [(0, (n, n, n), (0, pj, pi)), (1, (n, n, n), (0, pi)),
+                (2, (n, n, n), (0, pj))]
     if bp == BP1:
         # t-first stage order (hx_bp1.cu): X = (m, n, n) after the t
         # interpolation, read / written as k-lines by the HBM stages (pattern
@@ -279,6 +289,8 @@ def plan(bp, deg, target=TARGET_THREADS, qstage=False):
         ords = (0, 8)
     if bp == BP3 and deg in BP3_ORD4:
         ords = ords + (4,)
+    if bp == BP35 and deg in BP35_ORD:
+        ords = (0, 2, 4)
     if bp == BP1 and deg in BP1_CFAST:
         ords = ords + tuple(o | 8 for o in ords)
     best = None
