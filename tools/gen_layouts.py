@@ -57,10 +57,11 @@ BP1_CFAST = _degrees("HX_GEN_BP1_CFAST", {2, 4, 6, 8, 10, 12, 14})
 # 0.87, N=6 0.90 -> 0.92, N=8 0.78 -> 0.79, N=10 0.70 -> 0.72)
 BP3_KI = _degrees("HX_GEN_BP3_KI", {2, 4, 6, 8, 10, 12, 14})
 # BP3.0 degrees whose S2 / S8 i-lines may take the k-paired lane order (ORD
-# 4, conflict-free X / Y / Z at N=7 in the model).  Round 1 measured it 1-2 %
-# slower at N=7 (r11/r12); on the round-2 kernel it is +0.2 % at E=32768 and
-# E=97,336 (r2_59: shared wavefronts 40.5 M -> 38.9 M, conflicts 4.6 M -> 2.8 M)
-BP3_ORD4 = _degrees("HX_GEN_BP3_ORD4", {7})
+# 4, combined with ORD 8 where that applies).  Round 1 measured it 1-2 %
+# slower at N=7 (r11/r12); on the round-2 kernel: N=7 +0.2 % (r2_59: shared
+# wavefronts 40.5 M -> 38.9 M, conflicts 4.6 M -> 2.8 M), N=4 0.902 -> 0.910,
+# N=8 0.815 -> 0.821, N=10 0.724 -> 0.739 (ORD 12); N=12 -0.004 (r2_61)
+BP3_ORD4 = _degrees("HX_GEN_BP3_ORD4", {4, 7, 8, 10})
 # BP3.5 degrees whose S2 / S4 lines may take the k-fastest (ORD 2) or
 # k-paired (ORD 4, k-paired layouts) lane order; the k-line stages touch HBM
 # and keep i-fastest lanes.  Measured (r2_60, config 4): N=9 0.975 -> 0.985,
@@ -288,7 +289,7 @@ def plan(bp, deg, target=TARGET_THREADS, qstage=False):
     if bp == BP3 and m % 2 == 0 and deg in BP3_KI:
         ords = (0, 8)
     if bp == BP3 and deg in BP3_ORD4:
-        ords = ords + (4,)
+        ords = ords + tuple(o | 4 for o in ords)
     if bp == BP35 and deg in BP35_ORD:
         ords = (0, 2, 4)
     if bp == BP1 and deg in BP1_CFAST:
