@@ -91,8 +91,8 @@ int hx_repack_factors(const hx_plan* plan, const double* src, int64_t n_el, doub
  * The kernel is a programmatic dependent launch: it may start while the
  * previous kernel on `stream` retires, but issues nothing except L2 prefetch
  * hints before that kernel has completed -- plain stream order for every
- * read of q / factors and write of out (hx_apply_range and hx_apply_energy
- * likewise).                                                                */
+ * read of q / factors and write of out (hx_apply_range, hx_apply_energy and
+ * hx_apply_energy_dir likewise).                                            */
 int hx_apply(const hx_plan* plan, const double* q, const double* factors, double* out,
              int64_t n_el, int* status_flag, void* stream);
 
